@@ -1,0 +1,267 @@
+/*
+ * specpipe_b200 — C ABI of the B200-native PipeInfer hot path.
+ *
+ * The reference (``specpipe``, a pure-Python package) has no FFI; the
+ * boundary this library sits behind is its Python API.  Each
+ * entry point below names the reference function it replaces.  The Python
+ * host (``paper_2407_11798_b200``) binds these with ctypes; see
+ * INTEGRATION.md for the binding a reference maintainer would add.
+ *
+ * Conventions
+ *  - every function returns an ``int`` status (SP_OK or an SP_ERR_* code);
+ *  - all tensor arguments are caller-owned DEVICE pointers unless the name
+ *    says ``host``; nothing on the hot path allocates;
+ *  - ``stream`` is a ``cudaStream_t`` passed as ``void*``; work is enqueued,
+ *    never synchronised, except the explicitly blocking ``*_sync`` queries;
+ *  - numerical errors detected on the device (bad token id, position beyond
+ *    max_context, non-finite activations, NaN logits, coverage violations)
+ *    set bits in a sticky device error word that the host reads when it
+ *    collects a run's result (no per-layer host synchronisation).
+ *
+ * Build: nvcc -gencode arch=compute_100a,code=sm_100a (B200 only).
+ */
+#ifndef SPECPIPE_B200_H
+#define SPECPIPE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map to the reference's exception types) ------------ */
+enum {
+  SP_OK = 0,
+  SP_ERR_MODEL = 1,     /* ModelError      model.py:35-36      */
+  SP_ERR_CACHE = 2,     /* CacheError      kvcache.py:25-26    */
+  SP_ERR_PROTOCOL = 3,  /* ProtocolError   transport.py:34-35  */
+  SP_ERR_CUDA = 4,      /* CUDA runtime failure                 */
+  SP_ERR_ARG = 5,       /* invalid argument to the C ABI        */
+  SP_ERR_CAPACITY = 6   /* cell pool / descriptor capacity      */
+};
+
+/* ---- sticky device error bits ----------------------------------------- */
+enum {
+  SP_DEV_BAD_TOKEN = 1,      /* model.py:355-356 */
+  SP_DEV_BAD_POS = 2,        /* model.py:357-358, kvcache.py:142-143 */
+  SP_DEV_NONFINITE = 4,      /* model.py:419-420 */
+  SP_DEV_NAN_LOGITS = 8,     /* model.py:441-442 */
+  SP_DEV_COVERAGE = 16,      /* engine.py:625-633 */
+  SP_DEV_BAD_SEQ = 32,       /* kvcache.py:144-146 */
+  SP_DEV_PLAN_OVERFLOW = 64  /* visible list longer than the launch bound */
+};
+
+enum { SP_ARCH_REF = 0, SP_ARCH_LLAMA = 1 };
+enum { SP_DTYPE_F32 = 0, SP_DTYPE_BF16 = 1 };
+enum { SP_KIND_PREFILL = 0, SP_KIND_NONSPEC = 1, SP_KIND_SPEC = 2 };
+enum { SP_STATUS_VALID = 0, SP_STATUS_PLACEHOLDER = 1 };
+
+/* forward flags */
+enum {
+  SP_FWD_CHECK_COVERAGE = 1,  /* chain batches: token at pos p sees p cells */
+  SP_FWD_SKIPPABLE = 2,       /* speculative: honour cancel / placeholder  */
+  SP_FWD_CONTINUE = 4         /* same run, next layer sub-range: reuse the
+                                 descriptor, cells and plan (split
+                                 evaluation, model.py:5-11)               */
+};
+
+/* Model shape (ModelConfig, model.py:39-64, extended with the llama arch). */
+typedef struct sp_model_dims {
+  int32_t arch;        /* SP_ARCH_*                                     */
+  int32_t vocab;
+  int32_t d_model;
+  int32_t n_layers;
+  int32_t n_heads;
+  int32_t n_kv_heads;
+  int32_t head_dim;
+  int32_t ffn_dim;     /* ref: 4*d_model                                */
+  int32_t max_context;
+  int32_t w_dtype;     /* SP_DTYPE_* of weights and KV cache            */
+  float norm_eps;      /* ref: 1e-8 inside the mean; llama: 1e-5         */
+  float rope_theta;
+} sp_model_dims;
+
+/* One BatchToken (model.py:67-75); seq sets are bitmasks (P <= 32). */
+typedef struct sp_token {
+  int32_t token;
+  int32_t pos;
+  uint32_t seq_mask;
+  int32_t want_logits;
+} sp_token;
+
+/* Fused LM-head result per flagged row (model.py:438-457 on device). */
+typedef struct sp_row_result {
+  int32_t argmax;      /* greedy_sample: lowest id on ties   */
+  int32_t second;      /* second_best                         */
+  float conf;          /* max_softmax                         */
+  float max_logit;
+} sp_row_result;
+
+/* ======================================================================
+ * Low-level kernels
+ * ====================================================================== */
+
+/* K1: x[i] = E[tok_i] (+ P[pos_i] for the ref arch).  model.py:352-359 */
+int sp_embed(const sp_model_dims* dims, const void* emb, const float* pos_table,
+             const sp_token* toks, int n, float* x, int* err, void* stream);
+
+/* Epilogues of the weight-streaming GEMV family (K2/K6/K7/K9). */
+enum {
+  SP_EPI_STORE = 0,   /* y = norm(x) @ W^T                                  */
+  SP_EPI_RESID = 1,   /* out += x @ W^T (+ finite check)   model.py:416,418 */
+  SP_EPI_QKV = 2,     /* q -> out; k,v -> cache rows (+RoPE) model.py:387-393 */
+  SP_EPI_GELU = 3,    /* out = gelu(norm(x) @ W^T)          model.py:417-418 */
+  SP_EPI_SWIGLU = 4   /* out = silu(g)*u, rows interleaved (g,u)            */
+};
+
+typedef struct sp_gemv_args {
+  const void* w;          /* [n_rows, k] row-major, K contiguous          */
+  int32_t w_dtype;        /* SP_DTYPE_*                                   */
+  int32_t n_rows;
+  int32_t k;
+  const float* x;         /* [m, ldx]                                     */
+  int32_t m;
+  int32_t ldx;
+  int32_t norm;           /* fuse RMSNorm of x                           */
+  float norm_eps;
+  const float* gain;      /* optional RMSNorm gain [k]                   */
+  int32_t epi;            /* SP_EPI_*                                     */
+  void* out;              /* fp32 [m, ldo]                                */
+  int32_t ldo;
+  /* QKV epilogue */
+  int32_t q_rows;         /* rows [0,q_rows) -> q; then k; then v        */
+  int32_t kv_rows;
+  void* k_cache;          /* [cap, kv_rows] (w_dtype)                    */
+  void* v_cache;
+  int32_t cache_row0;     /* cell row of token 0; token i -> row0+i       */
+  int32_t rope;           /* rows are pair-interleaved per head          */
+  int32_t head_dim;
+  float rope_theta;
+  const sp_token* toks;   /* positions for RoPE                          */
+  int* err;
+  const int* run_state;   /* non-zero => skip (cancelled / placeholder)  */
+} sp_gemv_args;
+
+int sp_gemv(const sp_gemv_args* a, void* stream);
+
+/* K4: per query, the position-ordered visible cell rows (ties by row),
+ * the query's own row appended last.  model.py:287-323.  Rows >= row0
+ * are the batch's own cells (described by ``toks``).                     */
+int sp_build_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
+                  int n_old, int row0, const sp_token* toks, int n,
+                  int max_context, int32_t* vis, int32_t* vis_len, int ld_vis,
+                  int check_coverage, int* err, void* stream);
+
+/* K5: tree-masked attention over the plan.  model.py:394-415 */
+int sp_attention(const float* q, const void* k_cache, const void* v_cache,
+                 int kv_dtype, const int32_t* vis, const int32_t* vis_len,
+                 int ld_vis, int n, int n_heads, int n_kv_heads, int head_dim,
+                 int max_vis, float* out, float* scratch, int* tickets,
+                 const int* run_state, void* stream);
+
+/* K3/K10/K11: cell metadata (layer-uniform, one table per stage). */
+int sp_kv_meta_write(int32_t* cell_pos, uint32_t* cell_mask, int row0,
+                     const sp_token* toks, int n, int n_seq_ids,
+                     int max_context, int* err, void* stream);
+int sp_kv_copy(int32_t* cell_pos, uint32_t* cell_mask, int n_cells, int src,
+               uint32_t dst_mask, int end_pos, int max_context, void* stream);
+int sp_kv_remove(const int32_t* cell_pos, uint32_t* cell_mask, int n_cells,
+                 uint32_t seq_mask, int from_pos, void* stream);
+int sp_kv_keep(uint32_t* cell_mask, int n_cells, int seq, void* stream);
+
+/* K9: fused final RMSNorm + LM head + argmax/second/max-softmax. */
+int sp_lmhead(const void* w_out, int w_dtype, int vocab, int d, const float* x,
+              const int32_t* rows, int n_rows, int norm, float norm_eps,
+              const float* gain, sp_row_result* out, float* logits_out,
+              float* scratch, int* tickets, int* err, const int* run_state,
+              void* stream);
+
+/* ======================================================================
+ * Stage runtime: one pipeline stage (contiguous layer range) on one GPU.
+ * Replaces _Worker._on_activations + eval_layers (engine.py:563-623,
+ * model.py:326-421) and owns the stage's KV cells (kvcache.py:94-283).
+ * ====================================================================== */
+typedef struct sp_stage sp_stage;
+
+int sp_stage_create(const sp_model_dims* dims, int layer_lo, int layer_hi,
+                    int cell_capacity, int max_tokens, int n_seq_ids,
+                    sp_stage** out);
+int sp_stage_destroy(sp_stage* s);
+int sp_stage_set_embedding(sp_stage* s, const void* emb, const float* pos_table);
+int sp_stage_set_layer(sp_stage* s, int layer, const void* w_qkv,
+                       const void* w_o, const void* w_up, const void* w_down,
+                       const float* attn_norm, const float* mlp_norm);
+int sp_stage_set_head(sp_stage* s, const void* w_out, const float* final_norm);
+/* device-visible cancel words: table[run_id % size] == run_id => cancelled */
+int sp_stage_set_cancel_table(sp_stage* s, const int* table, int size);
+
+/* Enqueue layers [lo,hi) for one run.  ``host_toks`` is copied into a
+ * stream-ordered device descriptor (RUN_CONFIG, engine.py:231-251).
+ * ``x_in``: device activations (NULL on stage 0); ``in_status``: device
+ * status word of the upstream message (NULL if none).  ``x_out`` receives
+ * the stage output (the layers run in place on it) and ``out_status`` the
+ * placeholder flag (engine.py:545-554).  ``chain`` != 0: token 0 is the
+ * draft chain's tip argmax and the run is gated by the chain gate (the
+ * device-side speculate_microbatch loop, speculation.py:185-211). */
+int sp_stage_forward(sp_stage* s, const sp_token* host_toks, int n, int run_id,
+                     int kind, int flags, const float* x_in, const int* in_status,
+                     float* x_out, int* out_status, int chain, void* stream);
+
+/* Same, restricted to layers [layer_a, layer_b) of the stage (-1: all).
+ * With SP_FWD_CONTINUE the call continues the previous run of this stage. */
+int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks, int n,
+                           int run_id, int kind, int flags, const float* x_in,
+                           const int* in_status, float* x_out, int* out_status,
+                           int chain, int layer_a, int layer_b, void* stream);
+
+/* K9 over the flagged rows ``host_rows`` of ``x`` (the last forward's
+ * output): writes ``out[n_rows]``, optionally full logits, and a copy of the
+ * sticky error word into ``err_out``.  ``update_tip``: remember the last
+ * row's (argmax, conf) as the draft tip; ``chain_gate``: gate &= conf >=
+ * cutoff (one step of speculate_microbatch). */
+int sp_stage_lmhead(sp_stage* s, const float* x, const int32_t* host_rows,
+                    int n_rows, sp_row_result* out, float* logits_out,
+                    int* err_out, int update_tip, int chain_gate, float cutoff,
+                    void* stream);
+
+/* Draft chain: gate = tip.valid && tip.conf >= cutoff; out <- tip. */
+int sp_stage_chain_begin(sp_stage* s, float cutoff, sp_row_result* out,
+                         void* stream);
+int sp_stage_chain_state(sp_stage* s, int** tip, int** gate);
+/* SerialDecoder.truncate nulls the tip logits (model.py:507-512). */
+int sp_stage_invalidate_tip(sp_stage* s, void* stream);
+
+/* Sequence ops on the stage's cell table (CACHE_COPY / CACHE_REMOVE). */
+int sp_stage_cache_copy(sp_stage* s, int src, uint32_t dst_mask, int end_pos,
+                        void* stream);
+int sp_stage_cache_remove(sp_stage* s, int seq, int from_pos, void* stream);
+int sp_stage_cache_keep(sp_stage* s, int seq, void* stream);
+int sp_stage_reset(sp_stage* s, void* stream);
+/* Append cells (metadata only) — KVCache.insert for trace-replay tests. */
+int sp_stage_cache_insert_meta(sp_stage* s, const sp_token* host_toks, int n,
+                               void* stream);
+
+/* Queries (blocking, for tests/diagnostics and run-completion checks). */
+int sp_stage_n_cells(const sp_stage* s);
+int sp_stage_meta_sync(sp_stage* s, int32_t* host_pos, uint32_t* host_mask,
+                       int cap, void* stream);
+int sp_stage_read_kv_sync(sp_stage* s, int layer, int row, float* host_k,
+                          float* host_v, void* stream);
+int sp_stage_error_sync(sp_stage* s, int clear, void* stream);
+int sp_stage_error_ptr(sp_stage* s, int** dev_err);
+int sp_stage_plan_sync(sp_stage* s, int32_t* host_vis, int32_t* host_len,
+                       int n, void* stream);
+int sp_stage_ld_vis(const sp_stage* s);
+/* K4/K11: build the plan ``host_toks`` would get against the current table
+ * (without inserting its cells); visible counts = plan lengths - 1. */
+int sp_stage_plan_only(sp_stage* s, const sp_token* host_toks, int n,
+                       int check_coverage, void* stream);
+
+/* Library info. */
+const char* sp_version(void);
+int sp_device_arch(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECPIPE_B200_H */

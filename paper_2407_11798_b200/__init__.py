@@ -1,0 +1,70 @@
+"""paper_2407_11798_b200: B200-native PipeInfer hot path.
+
+Drop-in for the reference ``specpipe`` package's hot path (the public names
+of ``specpipe/__init__.py:3-58``), re-built on hand-written sm_100a kernels
+behind a C ABI (``include/specpipe_b200.h``).  No CPU fallback: compute
+entry points raise ``LibraryMissing`` if ``libspecpipe_b200.so`` is absent.
+"""
+
+from .errors import (  # noqa: F401
+    AllocationExhausted,
+    CacheError,
+    EngineError,
+    LibraryMissing,
+    ModelError,
+    ProtocolError,
+    SpeculationError,
+    TransportError,
+    VerifyError,
+)
+from .kvcache import KVCache, SequenceAllocator, free_sequence  # noqa: F401
+from .model import (  # noqa: F401
+    NON_SPECULATIVE,
+    PREFILL,
+    SPECULATIVE,
+    Batch,
+    BatchToken,
+    DeviceModel,
+    ModelConfig,
+    RowResult,
+    SerialDecoder,
+    build_model,
+    eval_layers,
+    greedy_sample,
+    llama_config,
+    logits,
+    max_softmax,
+    reference_decode,
+    sample_prompt,
+    second_best,
+)
+from .verify import (  # noqa: F401
+    VerifyResult,
+    apply_acceptance,
+    detect_stale_runs,
+    verify_run,
+)
+from .speculation import (  # noqa: F401
+    CutoffController,
+    DraftBackend,
+    SpeculationState,
+    SyntheticDraft,
+    ToyDraft,
+    rollback_draft,
+    speculate_microbatch,
+    sync_backend,
+)
+from .engine import (  # noqa: F401
+    ExperimentConfig,
+    RunMetrics,
+    RunRecord,
+    SimResult,
+    generate,
+    plan_layer_split,
+    simulate,
+    token_checksum,
+)
+
+LayeredModel = DeviceModel
+
+__version__ = "0.1.0"

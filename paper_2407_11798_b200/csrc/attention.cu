@@ -1,0 +1,341 @@
+// K4 + K5: visibility plan and tree-masked attention over the
+// sequence-partitioned cell table.
+//
+// Visibility rule (model.py:197-206, 287-323): query q sees cell c iff
+// c.pos < q.pos and c.seqs ∩ q.seqs ≠ ∅, plus itself.  The plan lists the
+// visible rows of each query in ascending position order (ties by row, which
+// equals the reference's cache-rows-then-batch-rows order because a run's
+// own cells are appended after every existing row), followed by the query's
+// own row.  It is built once per stage-run and reused by every layer of the
+// stage (the reference reuses its gather plans the same way, model.py:378-380).
+#include "kernels.cuh"
+
+namespace sp {
+
+constexpr int PLAN_THREADS = 512;
+
+// ---------------------------------------------------------------------------
+// K4: plan.  One CTA per query; counting sort over positions in smem.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PLAN_THREADS)
+plan_kernel(const int32_t* __restrict__ cell_pos,
+            const uint32_t* __restrict__ cell_mask, int n_old, int row0,
+            const sp_token* __restrict__ toks, int n, int max_context,
+            int32_t* __restrict__ vis, int32_t* __restrict__ vis_len,
+            int ld_vis, int check_cov, int* err) {
+  extern __shared__ int cnt[];  // [max_context + 1]
+  __shared__ int wsum[PLAN_THREADS / 32];
+  const int i = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int qpos = toks[i].pos;
+  const uint32_t qmask = toks[i].seq_mask;
+  const int P = max(0, min(qpos, max_context));
+  int32_t* out = vis + (size_t)i * ld_vis;
+
+  for (int p = tid; p <= P; p += PLAN_THREADS) cnt[p] = 0;
+  __syncthreads();
+  for (int r = tid; r < n_old; r += PLAN_THREADS) {
+    const int p = cell_pos[r];
+    if ((cell_mask[r] & qmask) && p < qpos) atomicAdd(&cnt[p], 1);
+  }
+  for (int j = tid; j < n; j += PLAN_THREADS) {
+    const int p = toks[j].pos;
+    if (j != i && (toks[j].seq_mask & qmask) && p < qpos) atomicAdd(&cnt[p], 1);
+  }
+  __syncthreads();
+
+  // exclusive scan of cnt[0..P) (each thread a contiguous segment)
+  const int seg = (P + PLAN_THREADS - 1) / PLAN_THREADS;
+  const int s0 = min(P, tid * seg), s1 = min(P, s0 + seg);
+  int local = 0;
+  for (int p = s0; p < s1; ++p) local += cnt[p];
+  const int lane = tid & 31, warp = tid >> 5;
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int wbase = 0;
+  for (int w = 0; w < warp; ++w) wbase += wsum[w];
+  int total = 0;
+  for (int w = 0; w < PLAN_THREADS / 32; ++w) total += wsum[w];
+  int run = wbase + incl - local;
+  __syncthreads();
+  for (int p = s0; p < s1; ++p) {
+    const int c = cnt[p];
+    cnt[p] = run;
+    run += c;
+  }
+  __syncthreads();
+
+  // place (cursor per position); ties are ordered afterwards
+  for (int r = tid; r < n_old; r += PLAN_THREADS) {
+    const int p = cell_pos[r];
+    if ((cell_mask[r] & qmask) && p < qpos) out[atomicAdd(&cnt[p], 1)] = r;
+  }
+  for (int j = tid; j < n; j += PLAN_THREADS) {
+    const int p = toks[j].pos;
+    if (j != i && (toks[j].seq_mask & qmask) && p < qpos)
+      out[atomicAdd(&cnt[p], 1)] = row0 + j;
+  }
+  __syncthreads();
+  // after placement cnt[p] is the END of position p's segment
+  for (int p = tid; p < P; p += PLAN_THREADS) {
+    const int b = p == 0 ? 0 : cnt[p - 1], e = cnt[p];
+    for (int a = b + 1; a < e; ++a) {  // insertion sort of a (tiny) tie run
+      const int v = out[a];
+      int c = a - 1;
+      while (c >= b && out[c] > v) { out[c + 1] = out[c]; --c; }
+      out[c + 1] = v;
+    }
+  }
+  if (tid == 0) {
+    out[total] = row0 + i;
+    vis_len[i] = total + 1;
+    if (check_cov && total != qpos) set_error(err, SP_DEV_COVERAGE);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: attention.  grid = (heads, queries, splits); each CTA takes up to
+// ATT_CH plan entries of one (query, head) and merges split partials in a
+// fixed order (last-arriving CTA), so results do not depend on scheduling.
+// ---------------------------------------------------------------------------
+constexpr int ATT_THREADS = 128;
+constexpr int ATT_CH = 128;
+constexpr int ATT_UNROLL = 4;
+
+
+
+template <typename T, int HD>
+__global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int LPR = HD / VEC;           // lanes per row
+  constexpr int G = ATT_THREADS / LPR;    // rows in flight per pass
+  static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "bad head dim");
+  __shared__ float sc[ATT_CH];
+  __shared__ float part[G][HD];
+  __shared__ float red[ATT_THREADS / 32];
+  __shared__ int last;
+
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 &&
+      a.cancel_word != nullptr && a.run_state_w != nullptr) {
+    // Early inference cancellation: observe the device-visible cancel word
+    // once per layer; every later kernel of this run reads run_state.
+    if (ld_volatile(a.cancel_word) == a.run_id) atomicExch(a.run_state_w, 1);
+  }
+  if (run_skipped(a.run_state)) return;
+
+  const int h = blockIdx.x, i = blockIdx.y, s = blockIdx.z;
+  const int len = a.vis_len[i];
+  const int ns = (len + ATT_CH - 1) / ATT_CH;
+  if (s == 0 && threadIdx.x == 0 && ns > a.nsplit) set_error(a.err, SP_DEV_PLAN_OVERFLOW);
+  if (s >= ns) return;
+  const int e0 = s * ATT_CH, e1 = min(len, e0 + ATT_CH);
+  const int kh = h / (a.H / a.KH);
+  const int kvd = a.KH * HD;
+  const int tid = threadIdx.x, g = tid / LPR, l = tid % LPR;
+  const int32_t* plan = a.vis + (size_t)i * a.ld_vis;
+  const T* Kc = reinterpret_cast<const T*>(a.k) + kh * HD + l * VEC;
+  const T* Vc = reinterpret_cast<const T*>(a.v) + kh * HD + l * VEC;
+
+  float qv[VEC];
+  {
+    const float* qp = a.q + (size_t)i * a.H * HD + h * HD + l * VEC;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) qv[j] = qp[j] * a.scale;
+  }
+
+  // scores
+  for (int eb = e0; eb < e1; eb += G * ATT_UNROLL) {
+    uint4 kv[ATT_UNROLL];
+#pragma unroll
+    for (int u = 0; u < ATT_UNROLL; ++u) {
+      const int e = eb + u * G + g;
+      const int row = e < e1 ? plan[e] : plan[e0];
+      kv[u] = ld_stream16(Kc + (size_t)row * kvd);
+    }
+#pragma unroll
+    for (int u = 0; u < ATT_UNROLL; ++u) {
+      float kf[VEC];
+      VecTraits<T>::unpack(kv[u], kf);
+      float d = 0.f;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) d = __fmaf_rn(qv[j], kf[j], d);
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      const int e = eb + u * G + g;
+      if (l == 0 && e < e1) sc[e - e0] = d;
+    }
+  }
+  __syncthreads();
+  const int cntv = e1 - e0;
+  float mx = -INFINITY;
+  for (int e = tid; e < cntv; e += ATT_THREADS) mx = fmaxf(mx, sc[e]);
+  mx = warp_max(mx);
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int w = 1; w < ATT_THREADS / 32; ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float sum = 0.f;
+  for (int e = tid; e < cntv; e += ATT_THREADS) {
+    const float p = __expf(sc[e] - mx);
+    sc[e] = p;
+    sum += p;
+  }
+  sum = warp_sum(sum);
+  if ((tid & 31) == 0) red[tid >> 5] = sum;
+  __syncthreads();
+  sum = red[0];
+#pragma unroll
+  for (int w = 1; w < ATT_THREADS / 32; ++w) sum += red[w];
+
+  // P @ V
+  float acc[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
+  for (int eb = e0; eb < e1; eb += G * ATT_UNROLL) {
+    uint4 vv[ATT_UNROLL];
+#pragma unroll
+    for (int u = 0; u < ATT_UNROLL; ++u) {
+      const int e = eb + u * G + g;
+      const int row = e < e1 ? plan[e] : plan[e0];
+      vv[u] = ld_stream16(Vc + (size_t)row * kvd);
+    }
+#pragma unroll
+    for (int u = 0; u < ATT_UNROLL; ++u) {
+      const int e = eb + u * G + g;
+      if (e < e1) {
+        float vf[VEC];
+        VecTraits<T>::unpack(vv[u], vf);
+        const float p = sc[e - e0];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[j] = __fmaf_rn(p, vf[j], acc[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) part[g][l * VEC + j] = acc[j];
+  __syncthreads();
+
+  float* outp = a.out + (size_t)i * a.H * HD + h * HD;
+  if (ns == 1) {
+    for (int d = tid; d < HD; d += ATT_THREADS) {
+      float o = part[0][d];
+      for (int gg = 1; gg < G; ++gg) o += part[gg][d];
+      outp[d] = o / sum;
+    }
+    return;
+  }
+  float* sp_ = a.scratch + (((size_t)i * a.H + h) * a.nsplit + s) * (HD + 2);
+  for (int d = tid; d < HD; d += ATT_THREADS) {
+    float o = part[0][d];
+    for (int gg = 1; gg < G; ++gg) o += part[gg][d];
+    sp_[2 + d] = o;
+  }
+  if (tid == 0) { sp_[0] = mx; sp_[1] = sum; }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const int t = atomicAdd(&a.tickets[i * a.H + h], 1);
+    last = (t == ns - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* base = a.scratch + ((size_t)i * a.H + h) * a.nsplit * (HD + 2);
+  float M = -INFINITY;
+  for (int ss = 0; ss < ns; ++ss) M = fmaxf(M, ld_volatile_f(base + ss * (HD + 2)));
+  float L = 0.f;
+  for (int ss = 0; ss < ns; ++ss) {
+    const float* b = base + ss * (HD + 2);
+    L += ld_volatile_f(b + 1) * __expf(ld_volatile_f(b) - M);
+  }
+  for (int d = tid; d < HD; d += ATT_THREADS) {
+    float o = 0.f;
+    for (int ss = 0; ss < ns; ++ss) {
+      const float* b = base + ss * (HD + 2);
+      o += ld_volatile_f(b + 2 + d) * __expf(ld_volatile_f(b) - M);
+    }
+    outp[d] = o / L;
+  }
+  if (tid == 0) a.tickets[i * a.H + h] = 0;
+}
+
+template <typename T>
+static cudaError_t attn_dispatch(const AttnArgs& a, int hd, cudaStream_t st) {
+  const dim3 grid(a.H, a.n, a.nsplit);
+  switch (hd) {
+    case 16: attn_kernel<T, 16><<<grid, ATT_THREADS, 0, st>>>(a); break;
+    case 32: attn_kernel<T, 32><<<grid, ATT_THREADS, 0, st>>>(a); break;
+    case 64: attn_kernel<T, 64><<<grid, ATT_THREADS, 0, st>>>(a); break;
+    case 128: attn_kernel<T, 128><<<grid, ATT_THREADS, 0, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
+                        int n_old, int row0, const sp_token* toks, int n,
+                        int max_context, int32_t* vis, int32_t* vis_len,
+                        int ld_vis, int check_cov, int* err, cudaStream_t st) {
+  const size_t smem = (size_t)(max_context + 1) * sizeof(int);
+  static int configured = 0;
+  if (smem > 48 * 1024 && configured < (int)smem) {
+    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = (int)smem;
+  }
+  plan_kernel<<<n, PLAN_THREADS, smem, st>>>(cell_pos, cell_mask, n_old, row0,
+                                             toks, n, max_context, vis, vis_len,
+                                             ld_vis, check_cov, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attention(const AttnArgs& a, int kv_dtype, int hd,
+                             cudaStream_t st) {
+  return kv_dtype == SP_DTYPE_BF16 ? attn_dispatch<__nv_bfloat16>(a, hd, st)
+                                   : attn_dispatch<float>(a, hd, st);
+}
+
+int attn_splits(int max_len) { return (max_len + ATT_CH - 1) / ATT_CH; }
+
+}  // namespace sp
+
+extern "C" int sp_build_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
+                             int n_old, int row0, const sp_token* toks, int n,
+                             int max_context, int32_t* vis, int32_t* vis_len,
+                             int ld_vis, int check_coverage, int* err,
+                             void* stream) {
+  if (n <= 0 || !toks || !vis || !vis_len) return SP_ERR_ARG;
+  return sp::launch_plan(cell_pos, cell_mask, n_old, row0, toks, n, max_context,
+                         vis, vis_len, ld_vis, check_coverage, err,
+                         reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SP_OK
+             : SP_ERR_CUDA;
+}
+
+extern "C" int sp_attention(const float* q, const void* k_cache,
+                            const void* v_cache, int kv_dtype,
+                            const int32_t* vis, const int32_t* vis_len,
+                            int ld_vis, int n, int n_heads, int n_kv_heads,
+                            int head_dim, int max_vis, float* out,
+                            float* scratch, int* tickets, const int* run_state,
+                            void* stream) {
+  if (n <= 0 || n_kv_heads <= 0 || n_heads % n_kv_heads) return SP_ERR_ARG;
+  sp::AttnArgs a{};
+  a.q = q; a.k = k_cache; a.v = v_cache; a.vis = vis; a.vis_len = vis_len;
+  a.ld_vis = ld_vis; a.n = n; a.H = n_heads; a.KH = n_kv_heads;
+  a.nsplit = sp::attn_splits(max_vis);
+  a.scale = 1.0f / sqrtf((float)head_dim);
+  a.out = out; a.scratch = scratch; a.tickets = tickets; a.run_state = run_state;
+  return sp::launch_attention(a, kv_dtype, head_dim,
+                              reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? SP_OK
+             : SP_ERR_ARG;
+}

@@ -1,0 +1,714 @@
+// Stage runtime: one pipeline stage (contiguous layer range) on one GPU.
+//
+// Replaces the stage worker's evaluation path (engine.py:563-623 calling
+// model.py:326-421): per run it enqueues, on one in-order stream,
+//   gate (cancel/placeholder/chain gate + cell metadata, K3/K14)
+//   embed (stage 0, K1) | activation copy
+//   plan (K4, once per stage-run, shared by all layers)
+//   per layer: QKV GEMV (+norm, RoPE, KV write) -> attention (K5)
+//              -> O GEMV (+residual) -> up GEMV (+norm, GELU/SwiGLU)
+//              -> down GEMV (+residual, finite check)
+//   epilogue (purge of skipped runs, placeholder status)
+// and never synchronises with the host.  Cell rows are handed out in run
+// order by the host, identically on every stage.
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cstring>
+
+#include "kernels.cuh"
+
+namespace sp {
+
+// ---- small kernels ---------------------------------------------------------
+
+// K1 (model.py:352-359): x[i] = E[tok] (+ P[pos]).
+template <typename T>
+__global__ void embed_kernel(const T* __restrict__ emb,
+                             const float* __restrict__ pos_table,
+                             const sp_token* __restrict__ toks, int n, int d,
+                             int vocab, int max_context, float* __restrict__ x,
+                             int* err, const int* run_state) {
+  if (run_skipped(run_state)) return;
+  const int i = blockIdx.x;
+  const sp_token t = toks[i];
+  const bool ok_t = t.token >= 0 && t.token < vocab;
+  const bool ok_p = t.pos >= 0 && t.pos < max_context;
+  if (threadIdx.x == 0) {
+    if (!ok_t) set_error(err, SP_DEV_BAD_TOKEN);
+    if (!ok_p) set_error(err, SP_DEV_BAD_POS);
+  }
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float v = ok_t ? to_f32(emb[(size_t)t.token * d + c]) : 0.f;
+    if (pos_table != nullptr && ok_p) v = __fadd_rn(v, pos_table[(size_t)t.pos * d + c]);
+    x[(size_t)i * d + c] = v;
+  }
+}
+
+// Stage-run prologue: fold cancel word / upstream placeholder / draft-chain
+// gate into run_state, take token 0 from the chain if asked, write metadata.
+__global__ void gate_kernel(sp_token* toks, int n, int kind, int flags,
+                            const int* cancel_word, int run_id,
+                            const int* in_status, const int* gate,
+                            const int* chain_tip, int* run_state,
+                            int32_t* cell_pos, uint32_t* cell_mask, int row0,
+                            int n_seq, int max_context, int* err) {
+  __shared__ int skip;
+  if (threadIdx.x == 0) {
+    int s = 0;
+    if ((flags & SP_FWD_SKIPPABLE) && kind == SP_KIND_SPEC) {
+      if (cancel_word && ld_volatile(cancel_word) == run_id) s = 1;
+      if (in_status && ld_volatile(in_status) == SP_STATUS_PLACEHOLDER) s = 1;
+    }
+    if (gate && ld_volatile(gate) == 0) s = 1;
+    if (chain_tip) toks[0].token = chain_tip[0];
+    *run_state = s;
+    skip = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const sp_token t = toks[i];
+    uint32_t m = t.seq_mask;
+    if (n_seq < 32) m &= (1u << n_seq) - 1;
+    cell_pos[row0 + i] = t.pos;
+    cell_mask[row0 + i] = skip ? 0u : m;
+  }
+}
+
+// Stage-run epilogue: a skipped/abandoned speculative run purges the
+// partitions it wrote under (engine.py:556-561, 581-585, 602-612) and its
+// own cells; the outgoing message is a placeholder (engine.py:545-554).
+__global__ void epilogue_kernel(const sp_token* toks, int n, const int* run_state,
+                                const int32_t* cell_pos, uint32_t* cell_mask,
+                                int n_cells, int row0, int* out_status) {
+  const int skip = ld_volatile(run_state);
+  if (!skip) {
+    if (out_status && blockIdx.x == 0 && threadIdx.x == 0) *out_status = SP_STATUS_VALID;
+    return;
+  }
+  uint32_t purge = 0;
+  for (int i = 0; i < n; ++i) purge |= toks[i].seq_mask;
+  purge &= ~1u;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_cells;
+       r += gridDim.x * blockDim.x) {
+    if (r >= row0 && r < row0 + n) cell_mask[r] = 0u;
+    else if (purge) cell_mask[r] &= ~purge;
+  }
+  if (out_status && blockIdx.x == 0 && threadIdx.x == 0) *out_status = SP_STATUS_PLACEHOLDER;
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ x, int d,
+                                   const int32_t* __restrict__ rows,
+                                   float* __restrict__ out, const int* run_state) {
+  if (run_skipped(run_state)) return;
+  const int r = blockIdx.x;
+  const float* src = x + (size_t)rows[r] * d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) out[(size_t)r * d + c] = src[c];
+}
+
+__global__ void chain_begin_kernel(const int* tip, int* gate, float cutoff,
+                                   sp_row_result* out) {
+  const int valid = tip[2];
+  const float conf = valid ? __int_as_float(tip[1]) : -1.0f;
+  *gate = (valid && conf >= cutoff) ? 1 : 0;
+  if (out) {
+    sp_row_result r;
+    r.argmax = valid ? tip[0] : -1;
+    r.second = -1;
+    r.conf = conf;
+    r.max_logit = 0.f;
+    *out = r;
+  }
+}
+
+}  // namespace sp
+
+using namespace sp;
+
+struct LayerW {
+  const void* qkv = nullptr;
+  const void* o = nullptr;
+  const void* up = nullptr;
+  const void* down = nullptr;
+  const float* attn_norm = nullptr;
+  const float* mlp_norm = nullptr;
+};
+
+static constexpr int DESC_RING = 64;
+
+struct sp_stage {
+  sp_model_dims dims{};
+  int lo = 0, hi = 0, cap = 0, max_tokens = 0, n_seq = 0;
+  int q_dim = 0, kv_dim = 0, up_rows = 0;
+  std::vector<LayerW> layers;
+  const void* emb = nullptr;
+  const float* pos_table = nullptr;
+  const void* w_out = nullptr;
+  const float* final_norm = nullptr;
+  const int* cancel_table = nullptr;
+  int cancel_size = 0;
+
+  int32_t* cell_pos = nullptr;
+  uint32_t* cell_mask = nullptr;
+  int n_cells = 0;
+  void* kc = nullptr;
+  void* vc = nullptr;
+  size_t kv_layer_elems = 0;
+
+  float* q = nullptr;
+  float* attn = nullptr;
+  float* h = nullptr;
+  float* xg = nullptr;
+  int32_t* vis = nullptr;
+  int32_t* vis_len = nullptr;
+  int ld_vis = 0;
+  float* att_scratch = nullptr;
+  size_t att_scratch_floats = 0;
+  int* att_tickets = nullptr;
+  LmPartial* lm_scratch = nullptr;
+  int* lm_ticket = nullptr;
+  int* err = nullptr;
+  int* run_state = nullptr;
+  int* tip = nullptr;   // [argmax, conf bits, valid]
+  int* gate = nullptr;
+
+  sp_token* desc_dev = nullptr;
+  sp_token* desc_host = nullptr;
+  int32_t* rows_dev = nullptr;
+  int32_t* rows_host = nullptr;
+  cudaEvent_t ev[DESC_RING];
+  int slot = 0;
+
+  // last forward (for lmhead row gathering and the epilogue)
+  const sp_token* cur_desc = nullptr;
+  int cur_n = 0;
+  int cur_row0 = 0;
+  int cur_max_pos = 0;
+  int cur_flags = 0;
+};
+
+static int cuda_status(cudaError_t e) { return e == cudaSuccess ? SP_OK : SP_ERR_CUDA; }
+#define SP_CHECK(call)                       \
+  do {                                       \
+    cudaError_t _e = (call);                 \
+    if (_e != cudaSuccess) return SP_ERR_CUDA; \
+  } while (0)
+
+static size_t wbytes(const sp_model_dims& d) { return d.w_dtype == SP_DTYPE_BF16 ? 2 : 4; }
+
+extern "C" int sp_stage_create(const sp_model_dims* dims, int layer_lo,
+                               int layer_hi, int cell_capacity, int max_tokens,
+                               int n_seq_ids, sp_stage** out) {
+  if (!dims || !out || layer_lo < 0 || layer_hi <= layer_lo ||
+      layer_hi > dims->n_layers || cell_capacity <= 0 || max_tokens <= 0 ||
+      n_seq_ids < 1 || n_seq_ids > 32)
+    return SP_ERR_ARG;
+  const sp_model_dims& d = *dims;
+  if (d.n_kv_heads <= 0 || d.n_heads % d.n_kv_heads || d.head_dim <= 0)
+    return SP_ERR_ARG;
+  if (d.head_dim != 16 && d.head_dim != 32 && d.head_dim != 64 && d.head_dim != 128)
+    return SP_ERR_ARG;
+  sp_stage* s = new sp_stage();
+  s->dims = d;
+  s->lo = layer_lo; s->hi = layer_hi;
+  s->cap = cell_capacity; s->max_tokens = max_tokens; s->n_seq = n_seq_ids;
+  s->q_dim = d.n_heads * d.head_dim;
+  s->kv_dim = d.n_kv_heads * d.head_dim;
+  s->up_rows = d.arch == SP_ARCH_LLAMA ? 2 * d.ffn_dim : d.ffn_dim;
+  s->layers.resize(layer_hi - layer_lo);
+  const int nl = layer_hi - layer_lo;
+  s->kv_layer_elems = (size_t)cell_capacity * s->kv_dim;
+  s->ld_vis = cell_capacity + 1;
+  const size_t wb = wbytes(d);
+  const int mt = max_tokens;
+  bool ok = true;
+  auto alloc = [&](void** p, size_t bytes) {
+    if (ok && cudaMalloc(p, bytes) != cudaSuccess) ok = false;
+    if (ok) cudaMemset(*p, 0, bytes);
+  };
+  alloc((void**)&s->cell_pos, sizeof(int32_t) * cell_capacity);
+  alloc((void**)&s->cell_mask, sizeof(uint32_t) * cell_capacity);
+  alloc(&s->kc, wb * s->kv_layer_elems * nl);
+  alloc(&s->vc, wb * s->kv_layer_elems * nl);
+  alloc((void**)&s->q, sizeof(float) * (size_t)mt * s->q_dim);
+  alloc((void**)&s->attn, sizeof(float) * (size_t)mt * s->q_dim);
+  alloc((void**)&s->h, sizeof(float) * (size_t)mt * d.ffn_dim);
+  alloc((void**)&s->xg, sizeof(float) * (size_t)mt * d.d_model);
+  alloc((void**)&s->vis, sizeof(int32_t) * (size_t)mt * s->ld_vis);
+  alloc((void**)&s->vis_len, sizeof(int32_t) * mt);
+  s->att_scratch_floats = (size_t)mt * d.n_heads *
+                          attn_splits(d.max_context + mt) * (d.head_dim + 2);
+  alloc((void**)&s->att_scratch, sizeof(float) * s->att_scratch_floats);
+  alloc((void**)&s->att_tickets, sizeof(int) * (size_t)mt * d.n_heads);
+  alloc((void**)&s->lm_scratch, sizeof(LmPartial) * (size_t)mt * lmhead_grid(d.vocab));
+  alloc((void**)&s->lm_ticket, sizeof(int));
+  alloc((void**)&s->err, sizeof(int));
+  alloc((void**)&s->run_state, sizeof(int));
+  alloc((void**)&s->tip, sizeof(int) * 4);
+  alloc((void**)&s->gate, sizeof(int));
+  alloc((void**)&s->desc_dev, sizeof(sp_token) * (size_t)mt * DESC_RING);
+  alloc((void**)&s->rows_dev, sizeof(int32_t) * (size_t)mt * DESC_RING);
+  if (ok && cudaMallocHost((void**)&s->desc_host, sizeof(sp_token) * (size_t)mt * DESC_RING) != cudaSuccess) ok = false;
+  if (ok && cudaMallocHost((void**)&s->rows_host, sizeof(int32_t) * (size_t)mt * DESC_RING) != cudaSuccess) ok = false;
+  for (int i = 0; ok && i < DESC_RING; ++i)
+    if (cudaEventCreateWithFlags(&s->ev[i], cudaEventDisableTiming) != cudaSuccess) ok = false;
+  if (ok) ok = cudaDeviceSynchronize() == cudaSuccess;
+  if (!ok) {
+    sp_stage_destroy(s);
+    return SP_ERR_CUDA;
+  }
+  *out = s;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_destroy(sp_stage* s) {
+  if (!s) return SP_OK;
+  cudaDeviceSynchronize();
+  void* ptrs[] = {s->cell_pos, s->cell_mask, s->kc, s->vc, s->q, s->attn, s->h,
+                  s->xg, s->vis, s->vis_len, s->att_scratch, s->att_tickets,
+                  s->lm_scratch, s->lm_ticket, s->err, s->run_state, s->tip,
+                  s->gate, s->desc_dev, s->rows_dev};
+  for (void* p : ptrs) if (p) cudaFree(p);
+  if (s->desc_host) cudaFreeHost(s->desc_host);
+  if (s->rows_host) cudaFreeHost(s->rows_host);
+  for (int i = 0; i < DESC_RING; ++i) if (s->ev[i]) cudaEventDestroy(s->ev[i]);
+  delete s;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_set_embedding(sp_stage* s, const void* emb,
+                                      const float* pos_table) {
+  if (!s) return SP_ERR_ARG;
+  s->emb = emb;
+  s->pos_table = pos_table;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_set_layer(sp_stage* s, int layer, const void* w_qkv,
+                                  const void* w_o, const void* w_up,
+                                  const void* w_down, const float* attn_norm,
+                                  const float* mlp_norm) {
+  if (!s || layer < s->lo || layer >= s->hi) return SP_ERR_ARG;
+  LayerW& L = s->layers[layer - s->lo];
+  L.qkv = w_qkv; L.o = w_o; L.up = w_up; L.down = w_down;
+  L.attn_norm = attn_norm; L.mlp_norm = mlp_norm;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_set_head(sp_stage* s, const void* w_out,
+                                 const float* final_norm) {
+  if (!s) return SP_ERR_ARG;
+  s->w_out = w_out;
+  s->final_norm = final_norm;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_set_cancel_table(sp_stage* s, const int* table, int size) {
+  if (!s || (table && size <= 0)) return SP_ERR_ARG;
+  s->cancel_table = table;
+  s->cancel_size = size;
+  return SP_OK;
+}
+
+static int next_slot(sp_stage* s) {
+  const int k = s->slot;
+  s->slot = (s->slot + 1) % DESC_RING;
+  cudaEventSynchronize(s->ev[k]);  // slot reuse: its H2D copy has completed
+  return k;
+}
+
+extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
+                                      int n, int run_id, int kind, int flags,
+                                      const float* x_in, const int* in_status,
+                                      float* x_out, int* out_status, int chain,
+                                      int layer_a, int layer_b, void* stream) {
+  if (!s || n <= 0 || !x_out) return SP_ERR_ARG;
+  if (layer_a < 0) { layer_a = s->lo; layer_b = s->hi; }
+  if (layer_a < s->lo || layer_b > s->hi || layer_b <= layer_a) return SP_ERR_MODEL;
+  const bool cont = (flags & SP_FWD_CONTINUE) != 0;
+  if (n > s->max_tokens) return SP_ERR_CAPACITY;
+  if (!cont && (!host_toks || s->n_cells + n > s->cap)) return SP_ERR_CAPACITY;
+  if (cont && (s->cur_desc == nullptr || s->cur_n != n)) return SP_ERR_PROTOCOL;
+  if (layer_a == 0 && !s->emb) return SP_ERR_ARG;
+  if (layer_a > 0 && !x_in) return SP_ERR_MODEL;  // model.py:361-362
+  for (int l = layer_a; l < layer_b; ++l)
+    if (!s->layers[l - s->lo].qkv) return SP_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const sp_model_dims& D = s->dims;
+  const int d = D.d_model;
+
+  sp_token* dd;
+  int row0, n_old, max_pos;
+  if (!cont) {
+    // RUN_CONFIG: stream-ordered descriptor (engine.py:231-251)
+    const int k = next_slot(s);
+    sp_token* hd = s->desc_host + (size_t)k * s->max_tokens;
+    dd = s->desc_dev + (size_t)k * s->max_tokens;
+    max_pos = 0;
+    for (int i = 0; i < n; ++i) {
+      hd[i] = host_toks[i];
+      max_pos = host_toks[i].pos > max_pos ? host_toks[i].pos : max_pos;
+    }
+    SP_CHECK(cudaMemcpyAsync(dd, hd, sizeof(sp_token) * n, cudaMemcpyHostToDevice, st));
+    SP_CHECK(cudaEventRecord(s->ev[k], st));
+    row0 = s->n_cells;
+    n_old = s->n_cells;
+    s->n_cells += n;
+    s->cur_desc = dd; s->cur_n = n; s->cur_row0 = row0; s->cur_max_pos = max_pos;
+    s->cur_flags = flags;
+  } else {
+    dd = const_cast<sp_token*>(s->cur_desc);
+    row0 = s->cur_row0;
+    n_old = row0;
+    max_pos = s->cur_max_pos;
+    flags = s->cur_flags | SP_FWD_CONTINUE;
+  }
+  const int* cancel_word = (s->cancel_table && (flags & SP_FWD_SKIPPABLE) &&
+                            kind == SP_KIND_SPEC)
+                               ? s->cancel_table + (run_id % s->cancel_size)
+                               : nullptr;
+  if (!cont) {
+    gate_kernel<<<1, 128, 0, st>>>(dd, n, kind, flags, cancel_word, run_id,
+                                   in_status, chain ? s->gate : nullptr,
+                                   chain ? s->tip : nullptr,
+                                   s->run_state, s->cell_pos, s->cell_mask, row0,
+                                   s->n_seq, D.max_context, s->err);
+    SP_CHECK(cudaGetLastError());
+  }
+
+  if (layer_a == 0) {
+    const int threads = d >= 256 ? 256 : 64;
+    if (D.w_dtype == SP_DTYPE_BF16)
+      embed_kernel<__nv_bfloat16><<<n, threads, 0, st>>>(
+          (const __nv_bfloat16*)s->emb, s->pos_table, dd, n, d, D.vocab,
+          D.max_context, x_out, s->err, s->run_state);
+    else
+      embed_kernel<float><<<n, threads, 0, st>>>(
+          (const float*)s->emb, s->pos_table, dd, n, d, D.vocab, D.max_context,
+          x_out, s->err, s->run_state);
+    SP_CHECK(cudaGetLastError());
+  } else if (x_in != x_out) {
+    SP_CHECK(cudaMemcpyAsync(x_out, x_in, sizeof(float) * (size_t)n * d,
+                             cudaMemcpyDeviceToDevice, st));
+  }
+
+  const int check = (flags & SP_FWD_CHECK_COVERAGE) ? 1 : 0;
+  if (!cont)
+    SP_CHECK(launch_plan(s->cell_pos, s->cell_mask, n_old, row0, dd, n,
+                         D.max_context, s->vis, s->vis_len, s->ld_vis, check,
+                         s->err, st));
+  // launch bound on visible entries per query (+ self): chain batches see
+  // exactly pos cells; otherwise bounded by the table size
+  const int bound = check ? (max_pos + 1) : (n_old + n);
+  const int nsplit = attn_splits(bound);
+  const size_t need = (size_t)n * D.n_heads * nsplit * (D.head_dim + 2);
+  if (need > s->att_scratch_floats) {
+    cudaStreamSynchronize(st);
+    cudaFree(s->att_scratch);
+    if (cudaMalloc((void**)&s->att_scratch, sizeof(float) * need) != cudaSuccess)
+      return SP_ERR_CUDA;
+    s->att_scratch_floats = need;
+  }
+
+  const bool llama = D.arch == SP_ARCH_LLAMA;
+  const size_t wb = wbytes(D);
+  for (int l = layer_a; l < layer_b; ++l) {
+    const LayerW& L = s->layers[l - s->lo];
+    void* kl = (char*)s->kc + wb * s->kv_layer_elems * (l - s->lo);
+    void* vl = (char*)s->vc + wb * s->kv_layer_elems * (l - s->lo);
+    sp_gemv_args g{};
+    g.w_dtype = D.w_dtype;
+    g.run_state = s->run_state;
+    g.err = s->err;
+    g.toks = dd;
+    g.m = n;
+    // q, k, v (model.py:387-393): rmsnorm fused, k/v into cell rows
+    g.w = L.qkv; g.n_rows = s->q_dim + 2 * s->kv_dim; g.k = d;
+    g.x = x_out; g.ldx = d; g.norm = 1; g.norm_eps = D.norm_eps;
+    g.gain = llama ? L.attn_norm : nullptr;
+    g.epi = SP_EPI_QKV; g.out = s->q; g.ldo = s->q_dim;
+    g.q_rows = s->q_dim; g.kv_rows = s->kv_dim; g.k_cache = kl; g.v_cache = vl;
+    g.cache_row0 = row0; g.rope = llama ? 1 : 0; g.head_dim = D.head_dim;
+    g.rope_theta = D.rope_theta;
+    int rc = sp_gemv(&g, stream);
+    if (rc) return rc;
+    // attention over the plan (model.py:394-415)
+    AttnArgs a{};
+    a.q = s->q; a.k = kl; a.v = vl; a.vis = s->vis; a.vis_len = s->vis_len;
+    a.ld_vis = s->ld_vis; a.n = n; a.H = D.n_heads; a.KH = D.n_kv_heads;
+    a.nsplit = nsplit; a.scale = 1.0f / sqrtf((float)D.head_dim);
+    a.out = s->attn; a.scratch = s->att_scratch; a.tickets = s->att_tickets;
+    a.run_state = s->run_state; a.run_state_w = s->run_state;
+    a.cancel_word = cancel_word; a.run_id = run_id; a.err = s->err;
+    SP_CHECK(launch_attention(a, D.w_dtype, D.head_dim, st));
+    // x += attn @ Wo (model.py:416)
+    g = sp_gemv_args{};
+    g.w_dtype = D.w_dtype; g.run_state = s->run_state; g.err = s->err; g.toks = dd;
+    g.m = n; g.w = L.o; g.n_rows = d; g.k = s->q_dim; g.x = s->attn; g.ldx = s->q_dim;
+    g.norm = 0; g.epi = SP_EPI_RESID; g.out = x_out; g.ldo = d;
+    rc = sp_gemv(&g, stream);
+    if (rc) return rc;
+    // h = act(rmsnorm(x) @ W1) (model.py:417-418)
+    g.w = L.up; g.n_rows = s->up_rows; g.k = d; g.x = x_out; g.ldx = d;
+    g.norm = 1; g.norm_eps = D.norm_eps; g.gain = llama ? L.mlp_norm : nullptr;
+    g.epi = llama ? SP_EPI_SWIGLU : SP_EPI_GELU; g.out = s->h; g.ldo = D.ffn_dim;
+    rc = sp_gemv(&g, stream);
+    if (rc) return rc;
+    // x += h @ W2 (+ finite check, model.py:418-420)
+    g.w = L.down; g.n_rows = d; g.k = D.ffn_dim; g.x = s->h; g.ldx = D.ffn_dim;
+    g.norm = 0; g.gain = nullptr; g.epi = SP_EPI_RESID; g.out = x_out; g.ldo = d;
+    rc = sp_gemv(&g, stream);
+    if (rc) return rc;
+  }
+  epilogue_kernel<<<max(1, min(148, (s->n_cells + 255) / 256)), 256, 0, st>>>(
+      dd, n, s->run_state, s->cell_pos, s->cell_mask, s->n_cells, row0, out_status);
+  SP_CHECK(cudaGetLastError());
+  return SP_OK;
+}
+
+extern "C" int sp_stage_forward(sp_stage* s, const sp_token* host_toks, int n,
+                                int run_id, int kind, int flags,
+                                const float* x_in, const int* in_status,
+                                float* x_out, int* out_status, int chain,
+                                void* stream) {
+  return sp_stage_forward_range(s, host_toks, n, run_id, kind,
+                                flags & ~SP_FWD_CONTINUE, x_in, in_status, x_out,
+                                out_status, chain, -1, -1, stream);
+}
+
+extern "C" int sp_stage_lmhead(sp_stage* s, const float* x,
+                               const int32_t* host_rows, int n_rows,
+                               sp_row_result* out, float* logits_out,
+                               int* err_out, int update_tip, int chain_gate,
+                               float cutoff, void* stream) {
+  if (!s || !x || !host_rows || n_rows <= 0 || !out) return SP_ERR_ARG;
+  if (s->hi != s->dims.n_layers || !s->w_out) return SP_ERR_ARG;
+  if (n_rows > s->max_tokens) return SP_ERR_CAPACITY;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const sp_model_dims& D = s->dims;
+  const int k = next_slot(s);
+  int32_t* hr = s->rows_host + (size_t)k * s->max_tokens;
+  int32_t* dr = s->rows_dev + (size_t)k * s->max_tokens;
+  for (int i = 0; i < n_rows; ++i) hr[i] = host_rows[i];
+  SP_CHECK(cudaMemcpyAsync(dr, hr, sizeof(int32_t) * n_rows, cudaMemcpyHostToDevice, st));
+  SP_CHECK(cudaEventRecord(s->ev[k], st));
+  gather_rows_kernel<<<n_rows, 128, 0, st>>>(x, D.d_model, dr, s->xg, s->run_state);
+  SP_CHECK(cudaGetLastError());
+  LmArgs a{};
+  a.w = s->w_out; a.V = D.vocab; a.d = D.d_model; a.x = s->xg; a.n_rows = n_rows;
+  a.norm = 1; a.eps = D.norm_eps;
+  a.gain = D.arch == SP_ARCH_LLAMA ? s->final_norm : nullptr;
+  a.out = out; a.logits = logits_out; a.scratch = s->lm_scratch;
+  a.ticket = s->lm_ticket; a.err = s->err; a.err_out = err_out;
+  a.run_state = s->run_state;
+  a.tip = update_tip ? s->tip : nullptr;
+  a.gate = update_tip ? s->gate : nullptr;
+  a.chain_gate = chain_gate;
+  a.cutoff = cutoff;
+  SP_CHECK(launch_lmhead(a, D.w_dtype, st));
+  return SP_OK;
+}
+
+extern "C" int sp_stage_chain_begin(sp_stage* s, float cutoff, sp_row_result* out,
+                                    void* stream) {
+  if (!s) return SP_ERR_ARG;
+  chain_begin_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      s->tip, s->gate, cutoff, out);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int sp_stage_chain_state(sp_stage* s, int** tip, int** gate) {
+  if (!s) return SP_ERR_ARG;
+  if (tip) *tip = s->tip;
+  if (gate) *gate = s->gate;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_invalidate_tip(sp_stage* s, void* stream) {
+  if (!s) return SP_ERR_ARG;
+  return cuda_status(cudaMemsetAsync(s->tip + 2, 0, sizeof(int),
+                                     reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int sp_stage_cache_copy(sp_stage* s, int src, uint32_t dst_mask,
+                                   int end_pos, void* stream) {
+  if (!s || src < 0 || src >= s->n_seq) return SP_ERR_CACHE;
+  if (s->n_seq < 32 && (dst_mask >> s->n_seq)) return SP_ERR_CACHE;
+  return cuda_status(launch_copy(s->cell_pos, s->cell_mask, s->n_cells, src,
+                                 dst_mask, end_pos, s->dims.max_context,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int sp_stage_cache_remove(sp_stage* s, int seq, int from_pos,
+                                     void* stream) {
+  if (!s || seq < 0 || seq >= s->n_seq) return SP_ERR_CACHE;
+  return cuda_status(launch_remove(s->cell_pos, s->cell_mask, s->n_cells,
+                                   1u << seq, from_pos,
+                                   reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int sp_stage_cache_keep(sp_stage* s, int seq, void* stream) {
+  if (!s || seq < 0 || seq >= s->n_seq) return SP_ERR_CACHE;
+  return cuda_status(launch_keep(s->cell_mask, s->n_cells, seq,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int sp_stage_cache_insert_meta(sp_stage* s, const sp_token* host_toks,
+                                          int n, void* stream) {
+  // test/diagnostic helper: append cells (metadata only, K/V untouched)
+  if (!s || !host_toks || n <= 0) return SP_ERR_ARG;
+  if (n > s->max_tokens || s->n_cells + n > s->cap) return SP_ERR_CAPACITY;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int k = next_slot(s);
+  sp_token* hd = s->desc_host + (size_t)k * s->max_tokens;
+  sp_token* dd = s->desc_dev + (size_t)k * s->max_tokens;
+  for (int i = 0; i < n; ++i) hd[i] = host_toks[i];
+  SP_CHECK(cudaMemcpyAsync(dd, hd, sizeof(sp_token) * n, cudaMemcpyHostToDevice, st));
+  SP_CHECK(cudaEventRecord(s->ev[k], st));
+  SP_CHECK(launch_meta_write(s->cell_pos, s->cell_mask, s->n_cells, dd, n,
+                             s->n_seq, s->dims.max_context, s->err, st));
+  s->n_cells += n;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_plan_only(sp_stage* s, const sp_token* host_toks, int n,
+                                  int check_coverage, void* stream) {
+  // K4/K11 query: the plan a batch WOULD get against the current table
+  // (visible rows per query, position order, own row last) without
+  // inserting its cells.  Read back with sp_stage_plan_sync.
+  if (!s || !host_toks || n <= 0) return SP_ERR_ARG;
+  if (n > s->max_tokens || s->n_cells + n > s->cap) return SP_ERR_CAPACITY;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int k = next_slot(s);
+  sp_token* hd = s->desc_host + (size_t)k * s->max_tokens;
+  sp_token* dd = s->desc_dev + (size_t)k * s->max_tokens;
+  for (int i = 0; i < n; ++i) hd[i] = host_toks[i];
+  SP_CHECK(cudaMemcpyAsync(dd, hd, sizeof(sp_token) * n, cudaMemcpyHostToDevice, st));
+  SP_CHECK(cudaEventRecord(s->ev[k], st));
+  SP_CHECK(launch_plan(s->cell_pos, s->cell_mask, s->n_cells, s->n_cells, dd, n,
+                       s->dims.max_context, s->vis, s->vis_len, s->ld_vis,
+                       check_coverage, s->err, st));
+  return SP_OK;
+}
+
+extern "C" int sp_stage_reset(sp_stage* s, void* stream) {
+  if (!s) return SP_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  SP_CHECK(cudaMemsetAsync(s->cell_mask, 0, sizeof(uint32_t) * s->cap, st));
+  SP_CHECK(cudaMemsetAsync(s->tip, 0, sizeof(int) * 4, st));
+  s->n_cells = 0;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_n_cells(const sp_stage* s) { return s ? s->n_cells : -1; }
+
+extern "C" int sp_stage_meta_sync(sp_stage* s, int32_t* host_pos,
+                                  uint32_t* host_mask, int cap, void* stream) {
+  if (!s || cap < s->n_cells) return SP_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (s->n_cells) {
+    SP_CHECK(cudaMemcpyAsync(host_pos, s->cell_pos, 4 * s->n_cells, cudaMemcpyDeviceToHost, st));
+    SP_CHECK(cudaMemcpyAsync(host_mask, s->cell_mask, 4 * s->n_cells, cudaMemcpyDeviceToHost, st));
+  }
+  SP_CHECK(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+extern "C" int sp_stage_read_kv_sync(sp_stage* s, int layer, int row,
+                                     float* host_k, float* host_v, void* stream) {
+  if (!s || layer < s->lo || layer >= s->hi || row < 0 || row >= s->cap)
+    return SP_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t wb = wbytes(s->dims);
+  const size_t off = wb * (s->kv_layer_elems * (layer - s->lo) + (size_t)row * s->kv_dim);
+  std::vector<uint16_t> tmp;
+  if (wb == 4) {
+    SP_CHECK(cudaMemcpyAsync(host_k, (char*)s->kc + off, 4 * s->kv_dim, cudaMemcpyDeviceToHost, st));
+    SP_CHECK(cudaMemcpyAsync(host_v, (char*)s->vc + off, 4 * s->kv_dim, cudaMemcpyDeviceToHost, st));
+    SP_CHECK(cudaStreamSynchronize(st));
+  } else {
+    tmp.resize(2 * s->kv_dim);
+    SP_CHECK(cudaMemcpyAsync(tmp.data(), (char*)s->kc + off, 2 * s->kv_dim, cudaMemcpyDeviceToHost, st));
+    SP_CHECK(cudaMemcpyAsync(tmp.data() + s->kv_dim, (char*)s->vc + off, 2 * s->kv_dim, cudaMemcpyDeviceToHost, st));
+    SP_CHECK(cudaStreamSynchronize(st));
+    for (int i = 0; i < s->kv_dim; ++i) {
+      uint32_t a = (uint32_t)tmp[i] << 16, b = (uint32_t)tmp[s->kv_dim + i] << 16;
+      memcpy(host_k + i, &a, 4);
+      memcpy(host_v + i, &b, 4);
+    }
+  }
+  return SP_OK;
+}
+
+extern "C" int sp_stage_error_sync(sp_stage* s, int clear, void* stream) {
+  if (!s) return -1;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int v = 0;
+  if (cudaMemcpyAsync(&v, s->err, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) return -1;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
+  if (clear) cudaMemsetAsync(s->err, 0, sizeof(int), st);
+  return v;
+}
+
+extern "C" int sp_stage_error_ptr(sp_stage* s, int** dev_err) {
+  if (!s || !dev_err) return SP_ERR_ARG;
+  *dev_err = s->err;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_plan_sync(sp_stage* s, int32_t* host_vis,
+                                  int32_t* host_len, int n, void* stream) {
+  if (!s || n <= 0 || n > s->max_tokens) return SP_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  SP_CHECK(cudaMemcpyAsync(host_len, s->vis_len, 4 * n, cudaMemcpyDeviceToHost, st));
+  SP_CHECK(cudaMemcpyAsync(host_vis, s->vis, 4 * (size_t)n * s->ld_vis, cudaMemcpyDeviceToHost, st));
+  SP_CHECK(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+extern "C" int sp_stage_ld_vis(const sp_stage* s) { return s ? s->ld_vis : -1; }
+
+extern "C" int sp_embed(const sp_model_dims* dims, const void* emb,
+                        const float* pos_table, const sp_token* toks, int n,
+                        float* x, int* err, void* stream) {
+  if (!dims || !emb || !toks || n <= 0 || !x) return SP_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int d = dims->d_model;
+  if (dims->w_dtype == SP_DTYPE_BF16)
+    embed_kernel<__nv_bfloat16><<<n, 128, 0, st>>>((const __nv_bfloat16*)emb, pos_table,
+                                                   toks, n, d, dims->vocab,
+                                                   dims->max_context, x, err, nullptr);
+  else
+    embed_kernel<float><<<n, 128, 0, st>>>((const float*)emb, pos_table, toks, n, d,
+                                           dims->vocab, dims->max_context, x, err,
+                                           nullptr);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int sp_lmhead(const void* w_out, int w_dtype, int vocab, int d,
+                         const float* x, const int32_t* rows, int n_rows, int norm,
+                         float norm_eps, const float* gain, sp_row_result* out,
+                         float* logits_out, float* scratch, int* tickets,
+                         int* err, const int* run_state, void* stream) {
+  // low-level form: ``rows`` must be NULL (x already holds the n_rows rows
+  // contiguously); ``scratch`` needs n_rows * ceil(vocab/8) * 32 bytes.
+  if (!w_out || !x || rows || n_rows <= 0 || !out || !scratch || !tickets)
+    return SP_ERR_ARG;
+  LmArgs a{};
+  a.w = w_out; a.V = vocab; a.d = d; a.x = x; a.n_rows = n_rows; a.norm = norm;
+  a.eps = norm_eps; a.gain = gain; a.out = out; a.logits = logits_out;
+  a.scratch = reinterpret_cast<LmPartial*>(scratch); a.ticket = tickets;
+  a.err = err; a.run_state = run_state;
+  return cuda_status(launch_lmhead(a, w_dtype, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" const char* sp_version(void) { return "specpipe_b200 0.1 sm_100a"; }
+
+extern "C" int sp_device_arch(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major * 10 + minor;
+}
