@@ -271,6 +271,7 @@ template <typename T>
 static cudaError_t attn_dispatch(const AttnArgs& a, int hd, cudaStream_t st) {
   const dim3 grid(a.H, a.n, a.nsplit);
   switch (hd) {
+    case 8: attn_kernel<T, 8><<<grid, ATT_THREADS, 0, st>>>(a); break;
     case 16: attn_kernel<T, 16><<<grid, ATT_THREADS, 0, st>>>(a); break;
     case 32: attn_kernel<T, 32><<<grid, ATT_THREADS, 0, st>>>(a); break;
     case 64: attn_kernel<T, 64><<<grid, ATT_THREADS, 0, st>>>(a); break;

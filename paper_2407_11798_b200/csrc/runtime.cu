@@ -207,7 +207,8 @@ extern "C" int sp_stage_create(const sp_model_dims* dims, int layer_lo,
   const sp_model_dims& d = *dims;
   if (d.n_kv_heads <= 0 || d.n_heads % d.n_kv_heads || d.head_dim <= 0)
     return SP_ERR_ARG;
-  if (d.head_dim != 16 && d.head_dim != 32 && d.head_dim != 64 && d.head_dim != 128)
+  if (d.head_dim != 8 && d.head_dim != 16 && d.head_dim != 32 && d.head_dim != 64 &&
+      d.head_dim != 128)
     return SP_ERR_ARG;
   sp_stage* s = new sp_stage();
   s->dims = d;

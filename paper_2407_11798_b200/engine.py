@@ -1,12 +1,160 @@
-"""Pipeline orchestration (placeholder while the engine is being ported)."""
+"""Pipeline orchestration on B200: configuration, layer split, the head's
+four decoding modes, metrics (mirror of ``specpipe/engine.py``).
+
+* ``iterative`` / ``pipeline-iterative`` — one non-speculative run at a time;
+* ``sync-speculative`` — draft round trip, then one verification chain;
+* ``async-speculative`` — PipeInfer: continuous asynchronous speculation
+  over FIFO sequence partitions with early inference cancellation.
+
+The head keeps the reference controller's decisions (engine.py:695-1273)
+with two deliberate fixes: F4(a) a speculative run launched
+while the frontier token is carried by an in-flight run copies its prefix
+from that run's partition; F4(b) a draft request whose context is a strict
+prefix of the draft's state backs off one token so the tip is recomputed.
+Runs execute on GPU stages (``pipeline.py`` / ``dist.py``); the draft on its
+own stream (``drafting.py``).  All times are host wall-clock seconds.
+"""
 
 from __future__ import annotations
 
 import hashlib
-from dataclasses import dataclass, field
+import time
+from collections import deque
+from dataclasses import dataclass, field, fields, replace
 from typing import Dict, List, Optional, Sequence, Tuple
 
-from .errors import EngineError
+import numpy as np
+
+from . import _lib
+from .errors import EngineError, ProtocolError
+from .kvcache import SequenceAllocator
+from .model import (KIND_CODE, NON_SPECULATIVE, PREFILL, SPECULATIVE, Batch,
+                    BatchToken, ModelConfig, encode_tokens, greedy_sample,
+                    llama_config, sample_prompt)
+from .speculation import CutoffController
+from .verify import INVALID, apply_acceptance, detect_stale_runs, verify_run
+
+MODES = ("iterative", "pipeline-iterative", "sync-speculative", "async-speculative")
+
+IN_FLIGHT = "in-flight"
+COMPLETED = "completed"
+CANCELLED_INVALID = "cancelled-invalid"
+CANCELLED_SUPERFLUOUS = "cancelled-superfluous"
+DRAINED = "drained"
+
+
+# ---------------------------------------------------------------------------
+# configuration
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class ExperimentConfig:
+    """One experiment (engine.py:80-183) plus B200 fields.
+
+    The simulator's delay knobs (``per_layer_delay``, ``link_latency``,
+    ``per_byte_delay``, ``draft_token_delay``) are accepted for drop-in
+    compatibility and ignored: costs are whatever the GPU takes.
+    """
+
+    mode: str = "async-speculative"
+    nodes: int = 8
+    vocab_size: int = 256
+    embed_dim: int = 64
+    target_layers: int = 12
+    draft_layers: int = 2
+    draft_embed_dim: int = 64
+    n_heads: int = 1
+    max_context: int = 1024
+    target_seed: int = 1
+    draft_seed: int = 2
+    draft_backend: str = "toy"
+    alpha: float = 0.8
+    cutoff: float = 0.4
+    cutoff_recovery: float = 0.05
+    cutoff_decay: float = 0.05
+    microbatch: int = 4
+    tree_cap: int = 4
+    continuous: bool = True
+    partitions: int = 8
+    prompt_seed: int = 1234
+    prompt_len: int = 128
+    gen_len: int = 512
+    clock: str = "wall"
+    repetitions: int = 1
+    per_layer_delay: float = 1e-3
+    link_latency: float = 1e-5
+    per_byte_delay: float = 0.0
+    draft_token_delay: float = 5e-4
+    idle_poll: float = 1e-4
+    eos_token: Optional[int] = None
+    node_weights: Optional[Tuple[int, ...]] = None
+    # --- B200 extensions ---
+    arch: str = "ref"                    # target/draft arch when no shape is named
+    target_shape: Optional[str] = None   # e.g. "llama2-7b" (model.LLAMA_SHAPES)
+    draft_shape: Optional[str] = None    # e.g. "llama-160m"
+    capacity: int = 8192                 # cell pool per stage
+    max_run_tokens: int = 256            # largest batch (prefill) per stage-run
+
+    def validate(self) -> None:
+        if self.mode not in MODES:
+            raise EngineError(f"unknown mode {self.mode!r}; expected one of {MODES}")
+        if self.clock not in ("virtual", "wall"):
+            raise EngineError(f"unknown clock {self.clock!r}")
+        if self.draft_backend not in ("toy", "synthetic"):
+            raise EngineError(f"unknown draft backend {self.draft_backend!r}")
+        if not 0.0 <= self.alpha <= 1.0:
+            raise EngineError("alpha must be in [0, 1]")
+        if self.nodes < 1:
+            raise EngineError("need at least one node")
+        if self.uses_draft() and self.nodes < 2:
+            raise EngineError(f"{self.mode} needs >= 2 nodes (one is the draft node)")
+        if not 1 <= self.microbatch <= 4:
+            raise EngineError("microbatch must be within [1, 4]")
+        if self.tree_cap < 1:
+            raise EngineError("tree_cap must be >= 1")
+        if self.partitions < 2:
+            raise EngineError("partitions must be >= 2")
+        if self.partitions > 32:
+            raise EngineError("partitions must be <= 32 (one mask bit each)")
+        if self.gen_len < 1 or self.prompt_len < 1:
+            raise EngineError("prompt_len and gen_len must be >= 1")
+        if self.prompt_len + self.gen_len > self.max_context:
+            raise EngineError("prompt_len + gen_len exceeds max_context")
+        if self.idle_poll <= 0:
+            raise EngineError("idle_poll must be > 0 (prevents zero-time spinning)")
+        if self.repetitions < 1:
+            raise EngineError("repetitions must be >= 1")
+        if self.prompt_len > self.max_run_tokens:
+            raise EngineError("prompt_len exceeds max_run_tokens")
+        self.target_config().validate()
+        if self.uses_draft():
+            self.draft_config().validate()
+
+    def uses_draft(self) -> bool:
+        return self.mode in ("sync-speculative", "async-speculative")
+
+    def target_config(self) -> ModelConfig:
+        if self.target_shape:
+            return llama_config(self.target_shape, self.max_context, self.target_seed)
+        return ModelConfig(vocab_size=self.vocab_size, embed_dim=self.embed_dim,
+                           n_layers=self.target_layers, n_heads=self.n_heads,
+                           max_context=self.max_context, seed=self.target_seed,
+                           arch=self.arch)
+
+    def draft_config(self) -> ModelConfig:
+        if self.draft_shape:
+            return llama_config(self.draft_shape, self.max_context, self.draft_seed)
+        return ModelConfig(vocab_size=self.vocab_size, embed_dim=self.draft_embed_dim,
+                           n_layers=self.draft_layers, n_heads=self.n_heads,
+                           max_context=self.max_context, seed=self.draft_seed,
+                           arch=self.arch)
+
+    def n_stages(self) -> int:
+        if self.mode == "iterative":
+            return 1
+        if self.uses_draft():
+            return self.nodes - 1
+        return self.nodes
 
 
 def plan_layer_split(n_layers: int, n_nodes: int,
@@ -44,12 +192,14 @@ def plan_layer_split(n_layers: int, n_nodes: int,
     return out
 
 
-def token_checksum(tokens: Sequence) -> str:
-    return hashlib.sha256(",".join(str(t) for t in tokens).encode()).hexdigest()
-
+# ---------------------------------------------------------------------------
+# records and metrics
+# ---------------------------------------------------------------------------
 
 @dataclass
 class RunRecord:
+    """Head-side state of one in-flight run (engine.py:339-360)."""
+
     run_id: int
     kind: str
     tokens: tuple
@@ -58,7 +208,7 @@ class RunRecord:
     seq_id: int
     logit_slots: Dict[int, int]
     basis: tuple = ()
-    status: str = "in-flight"
+    status: str = IN_FLIGHT
     launch_time: float = 0.0
     judged: int = 0
 
@@ -70,23 +220,721 @@ class RunRecord:
 
 
 @dataclass
-class ExperimentConfig:
-    pass
+class RunMetrics:
+    """Reference metric schema (engine.py:367-420)."""
+
+    mode: str
+    clock: str
+    tokens_generated: int
+    duration: float
+    generation_speed: float
+    ttft: float
+    itl: float
+    acceptance_rate: float
+    examined: int
+    matched: int
+    runs_started: int
+    spec_runs: int
+    cancelled_invalid: int
+    cancelled_superfluous: int
+    cancelled_runs: int
+    drained_runs: int
+    alloc_stalls: int
+    inflight_mean: float
+    bytes_by_tag: Dict[str, int]
+    msgs_by_tag: Dict[str, int]
+    token_checksum: str
+    virtual_end: float
+    wall_seconds: float
+
+    def to_dict(self, include_wall: bool = True) -> dict:
+        d = {f.name: getattr(self, f.name) for f in fields(self)}
+        d["bytes_by_tag"] = dict(sorted(self.bytes_by_tag.items()))
+        d["msgs_by_tag"] = dict(sorted(self.msgs_by_tag.items()))
+        if not include_wall:
+            d.pop("wall_seconds")
+        return d
 
 
 @dataclass
-class RunMetrics:
-    pass
+class CancelLogEntry:
+    run_id: int
+    reason: str
+    kind: str
+    min_pos: int
+    max_pos: int
+    accepted_len_at_cancel: int
+    chain: tuple
 
 
 @dataclass
 class SimResult:
-    pass
+    tokens: List[int]
+    metrics: RunMetrics
+    accepted_full: List[int]
+    accept_events: List[Tuple[float, int]]
+    cancel_log: List[CancelLogEntry]
+    node_logs: Dict[int, list]
+    consumed: Dict[Tuple[int, str], int]
+    sent: Dict[Tuple[int, str], int]
+    records: List[RunRecord]
 
 
-def simulate(cfg, **kw):
-    raise NotImplementedError
+def token_checksum(tokens: Sequence) -> str:
+    return hashlib.sha256(",".join(str(t) for t in tokens).encode()).hexdigest()
 
 
-def generate(*a, **kw):
-    raise NotImplementedError
+class _Inflight:
+    """Time-weighted mean of the FIFO depth (engine.py:451-467)."""
+
+    def __init__(self):
+        self.steps: List[Tuple[float, int]] = [(0.0, 0)]
+
+    def update(self, t: float, n: int) -> None:
+        self.steps.append((t, n))
+
+    def mean(self, start: float, end: float) -> float:
+        if end <= start:
+            return 0.0
+        tot = 0.0
+        for (t0, n), (t1, _) in zip(self.steps, self.steps[1:] + [(end, 0)]):
+            a, b = max(t0, start), min(t1, end)
+            if b > a:
+                tot += n * (b - a)
+        return tot / (end - start)
+
+
+# ---------------------------------------------------------------------------
+# the head
+# ---------------------------------------------------------------------------
+
+class Head:
+    """Sampling, verification, speculation and cancellation decisions."""
+
+    def __init__(self, cfg: ExperimentConfig, pipe, draft, prompt: List[int],
+                 d_model: int):
+        self.cfg = cfg
+        self.pipe = pipe
+        self.draft = draft
+        self.prompt = list(prompt)
+        self.d_model = d_model
+        self.accepted: List[int] = list(prompt)
+        self.run_counter = 0
+        self.fifo: deque = deque()
+        self.allocator = SequenceAllocator(cfg.partitions)
+        self.cutoff = CutoffController(base=cfg.cutoff, recovery=cfg.cutoff_recovery,
+                                       decay=cfg.cutoff_decay)
+        self.pending: List[Tuple[int, int]] = []
+        self.pending_tip_seq = 0
+        self.mirror: List[int] = []
+        self.request_ctx: Optional[List[int]] = None
+        self.draft_busy = False
+        self.spec_since_round = 0
+        self.idle_until = 0.0
+        self.generated = 0
+        self.terminal = False
+        self.window_start = 0.0
+        self.accept_events: List[Tuple[float, int]] = []
+        self.examined = self.matched = 0
+        self.runs_started = self.spec_runs = 0
+        self.cancelled_invalid = self.cancelled_superfluous = 0
+        self.drained_runs = self.alloc_stalls = 0
+        self._stalled = False
+        self.inflight = _Inflight()
+        self.cancel_log: List[CancelLogEntry] = []
+        self.records: List[RunRecord] = []
+        self.bytes: Dict[str, int] = {}
+        self.msgs: Dict[Tuple[int, str], int] = {}
+        self.stage_logs: Dict[int, list] = {i + 1: [] for i in range(pipe.n_stages)}
+        self._t0 = time.perf_counter()
+
+    def now(self) -> float:
+        return time.perf_counter() - self._t0
+
+    def _count(self, tag: str, nbytes: int, dst: int = 0, n: int = 1) -> None:
+        self.bytes[tag] = self.bytes.get(tag, 0) + nbytes
+        self.msgs[(dst, tag)] = self.msgs.get((dst, tag), 0) + n
+
+    # -- low-level helpers (engine.py:745-864) ------------------------------------
+    def _next_run_id(self) -> int:
+        self.run_counter += 1
+        return self.run_counter
+
+    def _launch(self, batch: Batch, seq_id: int, basis: tuple = ()) -> RunRecord:
+        rec = RunRecord(run_id=batch.run_id, kind=batch.kind,
+                        tokens=tuple(t.token for t in batch.tokens),
+                        min_pos=batch.tokens[0].pos, max_pos=batch.tokens[-1].pos,
+                        seq_id=seq_id,
+                        logit_slots={batch.tokens[i].pos: slot
+                                     for slot, i in enumerate(batch.logit_indices)},
+                        basis=basis, launch_time=self.now())
+        flags = _lib.SP_FWD_CHECK_COVERAGE
+        if batch.kind == SPECULATIVE:
+            flags |= _lib.SP_FWD_SKIPPABLE
+        self.pipe.launch(batch.run_id, KIND_CODE[batch.kind], encode_tokens(batch.tokens),
+                         flags, list(batch.logit_indices))
+        n = len(batch.tokens)
+        S = self.pipe.n_stages
+        self._count("RUN_CONFIG", (24 + 24 * n + 8 * sum(len(t.seqs) for t in batch.tokens) + 32) * S, 1, S)
+        self._count("ACTIVATIONS", (16 + 4 * n * self.d_model + 24) * max(0, S - 1), 2, max(0, S - 1))
+        for s in range(1, S + 1):
+            self.stage_logs[s].append(("run-config", batch.run_id))
+        self.fifo.append(rec)
+        self.records.append(rec)
+        self.runs_started += 1
+        if batch.kind == SPECULATIVE:
+            self.spec_runs += 1
+        self.inflight.update(self.now(), len(self.fifo))
+        return rec
+
+    def _emit_copy(self, src: int, dsts: Sequence[int], end_pos: int) -> None:
+        if dsts:
+            d = tuple(sorted(dsts))
+            self.pipe.copy(src, d, end_pos)
+            S = self.pipe.n_stages
+            self._count("CACHE_COPY", (24 + 8 * len(d) + 32) * S, 1, S)
+            for s in range(1, S + 1):
+                self.stage_logs[s].append(("cache-copy", src, d, end_pos))
+
+    def _emit_remove(self, seq: int, from_pos: int) -> None:
+        self.pipe.remove(seq, from_pos)
+        S = self.pipe.n_stages
+        self._count("CACHE_REMOVE", (24 + 32) * S, 1, S)
+        for s in range(1, S + 1):
+            self.stage_logs[s].append(("cache-remove", seq, from_pos))
+
+    def _accept(self, tok: int) -> None:
+        if self.generated >= self.cfg.gen_len or self.terminal:
+            return
+        self.accepted.append(tok)
+        self.generated += 1
+        self.accept_events.append((self.now(), tok))
+        if self.cfg.eos_token is not None and tok == self.cfg.eos_token:
+            self.terminal = True
+
+    def _judge_walked(self, rec: RunRecord, result) -> None:
+        """engine.py:809-823"""
+        if rec.kind != SPECULATIVE:
+            return
+        ok = result.matched_end - rec.min_pos
+        adjudicated = ok + (1 if result.mismatch else 0)
+        self.matched += max(0, ok - rec.judged)
+        self.examined += max(0, adjudicated - rec.judged)
+        rec.judged = max(rec.judged, adjudicated)
+
+    def _judge_cancelled(self, rec: RunRecord) -> None:
+        """engine.py:825-848"""
+        if rec.kind != SPECULATIVE:
+            return
+        for pos, tok in rec.basis:
+            if pos < len(self.accepted) and tok != self.accepted[pos]:
+                return
+        i = rec.judged
+        while i < len(rec.tokens):
+            pos = rec.min_pos + i
+            if pos >= len(self.accepted):
+                break
+            self.examined += 1
+            same = rec.tokens[i] == self.accepted[pos]
+            if same:
+                self.matched += 1
+            i += 1
+            if not same:
+                break
+        rec.judged = i
+
+    def _pop_record(self, res) -> RunRecord:
+        if not self.fifo:
+            raise ProtocolError(f"logits for run {res.run_id} with empty FIFO")
+        rec = self.fifo.popleft()
+        if rec.run_id != res.run_id:
+            raise ProtocolError(f"logits out of order: got run {res.run_id}, "
+                                f"expected {rec.run_id}")
+        self._count("LOGITS", 16 + 24 + 16 * len(res.rows), 0)
+        for s, st in enumerate(res.stage_status, start=1):
+            self.stage_logs[s].append(
+                ("evaluated" if st == _lib.SP_STATUS_VALID else "skip-or-abandon",
+                 res.run_id))
+        self.inflight.update(self.now(), len(self.fifo))
+        if res.err:
+            _lib.raise_device_error(res.err, f"run {res.run_id}")
+        if res.placeholder and rec.status == IN_FLIGHT:
+            raise ProtocolError(f"run {rec.run_id} came back as a placeholder "
+                                "without being cancelled")
+        return rec
+
+    def _recv(self):
+        return self.pipe.wait()
+
+    # -- draft requests -------------------------------------------------------------
+    def _draft_request(self, truncate_to: int, feed: Sequence[int], max_tokens: int,
+                       cutoff: float) -> None:
+        self.draft.request(truncate_to, feed, max_tokens, cutoff)
+        self._count("DRAFT_REQUEST", 24 + 32 + 8 * len(feed), self.cfg.nodes)
+        self.draft_busy = True
+
+    def _draft_reply(self):
+        toks, confs = self.draft.reply()
+        self.draft_busy = False
+        self._count("DRAFT_REPLY", 24 + 8 + 16 * len(toks), 0)
+        return toks, confs
+
+    # -- prefill (engine.py:868-900) ---------------------------------------------------
+    def _prefill(self) -> int:
+        if self.draft is not None:
+            self._draft_request(0, tuple(self.prompt), 0, 1.0)
+            self.mirror = list(self.prompt)
+        batch = Batch(tokens=tuple(BatchToken(t, i, frozenset([0]), i == len(self.prompt) - 1)
+                                   for i, t in enumerate(self.prompt)),
+                      kind=PREFILL, run_id=self._next_run_id())
+        rec = self._launch(batch, seq_id=0)
+        res = self._recv()
+        self._pop_record(res)
+        rec.status = COMPLETED
+        if self.draft is not None:
+            self._draft_reply()
+        t0 = greedy_sample(res.rows[0])
+        self.accepted.append(t0)
+        self.generated += 1
+        if self.cfg.eos_token is not None and t0 == self.cfg.eos_token:
+            self.terminal = True
+        self.window_start = self.now()
+        return t0
+
+    def _launch_ns(self, token: int, with_copy: bool) -> RunRecord:
+        pos = len(self.accepted) - 1
+        batch = Batch(tokens=(BatchToken(token, pos, frozenset([0]), True),),
+                      kind=NON_SPECULATIVE, run_id=self._next_run_id())
+        rec = self._launch(batch, seq_id=0)
+        if with_copy:
+            # early cache-entry sharing: canonical cells reach every partition
+            # right behind the run (engine.py:912-916, PAPER.md:485-496)
+            self._emit_copy(0, self.allocator.all_ids(), pos + 1)
+        return rec
+
+    # -- modes ---------------------------------------------------------------------
+    def run_iterative(self) -> None:
+        tok = self._prefill()
+        while self.generated < self.cfg.gen_len and not self.terminal:
+            self._launch_ns(tok, with_copy=False)
+            res = self._recv()
+            got = self._pop_record(res)
+            got.status = COMPLETED
+            result = verify_run(got, res.rows, self.accepted, eos_token=self.cfg.eos_token)
+            if result.next_token is None:
+                raise ProtocolError("iterative run produced no next token")
+            self._accept(result.next_token)
+            tok = result.next_token
+        self._finish()
+
+    def run_sync_speculative(self) -> None:
+        tok = self._prefill()
+        while self.generated < self.cfg.gen_len and not self.terminal:
+            drafts, _ = self._draft_round_trip(self.cfg.tree_cap, self.cutoff.base)
+            pos = len(self.accepted) - 1
+            toks = [BatchToken(tok, pos, frozenset([0]), True)]
+            toks += [BatchToken(d, pos + 1 + i, frozenset([0]), True)
+                     for i, d in enumerate(drafts)]
+            batch = Batch(tokens=tuple(toks), kind=SPECULATIVE, run_id=self._next_run_id())
+            rec = self._launch(batch, seq_id=0)
+            rec.judged = 1   # the leading token is accepted context, not a draft
+            res = self._recv()
+            got = self._pop_record(res)
+            got.status = COMPLETED
+            result = verify_run(got, res.rows, self.accepted, eos_token=self.cfg.eos_token)
+            self._judge_walked(got, result)
+            for t in result.accepted:
+                self._accept(t)
+            if result.next_token is not None:
+                self._accept(result.next_token)
+            if result.mismatch:
+                self._emit_remove(0, result.matched_end)
+            if self.terminal:
+                break
+            tok = self.accepted[-1]
+        self._finish()
+
+    def run_async_speculative(self) -> None:
+        self._prefill()
+        if not (self.generated >= self.cfg.gen_len or self.terminal):
+            self._launch_ns(self.accepted[-1], with_copy=True)
+        while self.generated < self.cfg.gen_len and not self.terminal:
+            if self.pipe.ready():
+                self._handle_completion(self.pipe.poll())
+                continue
+            if self.draft_busy and self.draft.ready():
+                self._handle_reply(*self._draft_reply())
+                continue
+            if not self.draft_busy and self._want_speculation():
+                self._send_draft_request()
+                continue
+            self._block_until_message()
+        self._finish()
+
+    def _block_until_message(self) -> None:
+        """recv_any([LOGITS, DRAFT_REPLY]) without consuming (the loop does)."""
+        if self.pipe.in_flight() == 0 and not self.draft_busy:
+            raise EngineError("deadlock: nothing in flight and nothing to launch")
+        while True:
+            if self.pipe.ready() or (self.draft_busy and self.draft.ready()):
+                return
+            time.sleep(0)
+
+    # -- async internals (engine.py:1002-1182) -----------------------------------------
+    def _want_speculation(self) -> bool:
+        if self.terminal or self.generated >= self.cfg.gen_len:
+            return False
+        if not self.cfg.continuous and self.spec_since_round >= 1:
+            return False
+        if self.allocator.available() == 0:
+            if not self._stalled:
+                self._stalled = True
+                self.alloc_stalls += 1
+            return False
+        self._stalled = False
+        if self.now() < self.idle_until:
+            return False
+        return len(self.accepted) + len(self.pending) + 1 <= self.cfg.max_context
+
+    @staticmethod
+    def _common_prefix(a: Sequence[int], b: Sequence[int]) -> int:
+        n = 0
+        for x, y in zip(a, b):
+            if x != y:
+                break
+            n += 1
+        return n
+
+    def _backoff(self, cp: int, ctx: List[int]) -> Tuple[int, List[int]]:
+        """F4(b): a context that is a strict prefix of the draft's state would
+        truncate the draft without re-feeding anything, leaving it without
+        tip logits; back off one token and re-feed it."""
+        feed = ctx[cp:]
+        if not feed and cp < len(self.mirror) and cp > 0:
+            return cp - 1, ctx[cp - 1:]
+        return cp, feed
+
+    def _send_draft_request(self) -> None:
+        ctx = self.accepted + [t for _, t in self.pending]
+        cp = self._common_prefix(self.mirror, ctx)
+        if self.cfg.continuous:
+            cap = min(self.cfg.microbatch, max(1, len(self.pending)))
+        else:
+            cap = self.cfg.tree_cap
+        cap = min(cap, 4, self.cfg.max_context - len(ctx))
+        truncate_to, feed = self._backoff(cp, ctx)
+        self._draft_request(truncate_to, tuple(feed), cap, self.cutoff.current)
+        self.mirror = list(ctx)
+        self.request_ctx = list(ctx)
+
+    def _handle_reply(self, toks, confs) -> None:
+        props = list(toks)
+        self.mirror.extend(props)
+        ctx = self.accepted + [t for _, t in self.pending]
+        if self.request_ctx != ctx:
+            self.request_ctx = None
+            return
+        self.request_ctx = None
+        if not props:
+            if not self.pipe.ready():
+                self.cutoff.on_speculation_idle()
+            self.idle_until = self.now() + self.cfg.idle_poll
+            return
+        self.cutoff.note_success()
+        self._launch_spec(props)
+        self.spec_since_round += 1
+
+    def _carrier_seq(self) -> int:
+        """F4(a): partition of the in-flight run carrying the frontier token."""
+        pos = len(self.accepted) - 1
+        tok = self.accepted[-1]
+        for rec in self.fifo:
+            if (rec.status == IN_FLIGHT and rec.min_pos <= pos <= rec.max_pos
+                    and rec.tokens[pos - rec.min_pos] == tok):
+                return rec.seq_id
+        return 0
+
+    def _launch_spec(self, props: List[int]) -> None:
+        base = len(self.accepted) + len(self.pending)
+        seq = self.allocator.alloc()
+        src = self.pending_tip_seq if self.pending else self._carrier_seq()
+        self._emit_copy(src, (seq,), base)
+        basis = tuple(self.pending)
+        toks = tuple(BatchToken(t, base + i, frozenset([seq]), True)
+                     for i, t in enumerate(props))
+        batch = Batch(tokens=toks, kind=SPECULATIVE, run_id=self._next_run_id())
+        self._launch(batch, seq_id=seq, basis=basis)
+        self.pending.extend((base + i, t) for i, t in enumerate(props))
+        self.pending_tip_seq = seq
+
+    def _handle_completion(self, res) -> None:
+        rec = self._pop_record(res)
+        if rec.status in (CANCELLED_INVALID, CANCELLED_SUPERFLUOUS, DRAINED):
+            if rec.seq_id != 0:
+                self._emit_remove(rec.seq_id, 0)
+                self.allocator.free(rec.seq_id)
+            return
+        rec.status = COMPLETED
+        result = verify_run(rec, res.rows, self.accepted, eos_token=self.cfg.eos_token)
+        self._judge_walked(rec, result)
+        new_tokens = list(result.accepted)
+        if result.next_token is not None:
+            new_tokens.append(result.next_token)
+        for t in new_tokens:
+            self._accept(t)
+        cmds: List[Tuple[str, tuple]] = []
+        apply_acceptance(result, rec, lambda op, args: cmds.append((op, args)),
+                         self.allocator.live())
+        for op, args in cmds:
+            if op == "copy":
+                self._emit_copy(*args)
+            else:
+                self._emit_remove(*args)
+        if rec.seq_id != 0:
+            self.allocator.free(rec.seq_id)
+        if not new_tokens:
+            return
+        self._rebase_pending()
+        self.cutoff.on_run_accepted()
+        self.spec_since_round = 0
+        self._cancel_stale()
+        if self.generated < self.cfg.gen_len and not self.terminal:
+            if not self._frontier_carried():
+                self._launch_ns(self.accepted[-1], with_copy=True)
+
+    def _frontier_carried(self) -> bool:
+        pos = len(self.accepted) - 1
+        tok = self.accepted[-1]
+        return any(rec.status == IN_FLIGHT and rec.min_pos <= pos <= rec.max_pos
+                   and rec.tokens[pos - rec.min_pos] == tok for rec in self.fifo)
+
+    def _rebase_pending(self) -> None:
+        kept: List[Tuple[int, int]] = []
+        broken = False
+        for pos, tok in self.pending:
+            if pos < len(self.accepted):
+                if tok != self.accepted[pos]:
+                    broken = True
+                    break
+                continue
+            kept.append((pos, tok))
+        self.pending = [] if broken else kept
+        if not self.pending:
+            self.pending_tip_seq = 0
+
+    def _cancel_stale(self) -> None:
+        for rec, reason in detect_stale_runs(self.fifo, self.accepted):
+            rec.status = CANCELLED_INVALID if reason == INVALID else CANCELLED_SUPERFLUOUS
+            self._judge_cancelled(rec)
+            if reason == INVALID:
+                self.cancelled_invalid += 1
+            else:
+                self.cancelled_superfluous += 1
+            self.cancel_log.append(CancelLogEntry(
+                rec.run_id, reason, rec.kind, rec.min_pos, rec.max_pos,
+                len(self.accepted), tuple(rec.chain())))
+            self.pipe.cancel_run(rec.run_id)
+            self._count("CANCEL", (24 + 16) * self.pipe.n_stages, 1, self.pipe.n_stages)
+
+    # -- shutdown ------------------------------------------------------------------
+    def _finish(self) -> None:
+        for rec in self.fifo:
+            if rec.status == IN_FLIGHT:
+                rec.status = DRAINED
+                self.drained_runs += 1
+                self.pipe.cancel_run(rec.run_id)
+        while self.fifo:
+            res = self._recv()
+            rec = self._pop_record(res)
+            if rec.seq_id != 0 and rec.seq_id in self.allocator.live():
+                self.allocator.free(rec.seq_id)
+        if self.draft_busy:
+            self._draft_reply()
+
+    def _draft_round_trip(self, max_tokens: int, cutoff: float):
+        ctx = list(self.accepted)
+        cp = self._common_prefix(self.mirror, ctx)
+        room = self.cfg.max_context - len(ctx)
+        truncate_to, feed = self._backoff(cp, ctx)
+        self._draft_request(truncate_to, tuple(feed), max(0, min(max_tokens, room)), cutoff)
+        self.mirror = ctx
+        toks, confs = self._draft_reply()
+        self.mirror.extend(toks)
+        return toks, confs
+
+    # -- metrics (engine.py:1234-1273) ---------------------------------------------
+    def build_metrics(self, wall_seconds: float) -> RunMetrics:
+        times = [t for t, _ in self.accept_events]
+        k = len(times)
+        if k:
+            duration = times[-1] - self.window_start
+            ttft = times[0] - self.window_start
+            gaps = [b - a for a, b in zip(times, times[1:])]
+            itl = sum(gaps) / len(gaps) if gaps else 0.0
+            speed = k / duration if duration > 0 else float("inf")
+        else:
+            duration = ttft = itl = speed = 0.0
+        out = self.accepted[len(self.prompt):]
+        msgs: Dict[str, int] = {}
+        for (_, tag), n in self.msgs.items():
+            msgs[tag] = msgs.get(tag, 0) + n
+        return RunMetrics(
+            mode=self.cfg.mode, clock="wall", tokens_generated=len(out),
+            duration=duration, generation_speed=speed, ttft=ttft, itl=itl,
+            acceptance_rate=(self.matched / self.examined) if self.examined else 0.0,
+            examined=self.examined, matched=self.matched,
+            runs_started=self.runs_started, spec_runs=self.spec_runs,
+            cancelled_invalid=self.cancelled_invalid,
+            cancelled_superfluous=self.cancelled_superfluous,
+            cancelled_runs=self.cancelled_invalid + self.cancelled_superfluous,
+            drained_runs=self.drained_runs, alloc_stalls=self.alloc_stalls,
+            inflight_mean=self.inflight.mean(self.window_start,
+                                             times[-1] if k else self.window_start),
+            bytes_by_tag=dict(self.bytes), msgs_by_tag=msgs,
+            token_checksum=token_checksum(out), virtual_end=self.now(),
+            wall_seconds=wall_seconds)
+
+
+# ---------------------------------------------------------------------------
+# engine: models + pipeline + draft kept resident across runs
+# ---------------------------------------------------------------------------
+
+def truth_table(target_model, prompt: List[int], n: int):
+    """Target greedy stream and runner-ups along it (for the synthetic draft).
+
+    ``truth[p]``/``runner[p]`` are the greedy token and runner-up predicted
+    for absolute position p given the true context [0, p)."""
+    from .model import SerialDecoder
+    cfg = target_model.config
+    n = min(n, cfg.max_context - len(prompt))
+    dec = SerialDecoder(target_model, capacity=cfg.max_context + 64)
+    tip = dec.feed(prompt)
+    truth, runner = list(prompt), [0] * len(prompt)
+    for _ in range(n):
+        truth.append(tip.argmax)
+        runner.append(tip.second)
+        if len(dec) + 1 >= cfg.max_context:
+            break
+        tip = dec.feed([tip.argmax])
+    del dec
+    return truth, runner
+
+
+class Engine:
+    """Keeps the GPU-resident models, stages and draft server for a config."""
+
+    def __init__(self, cfg: ExperimentConfig, target_model=None, draft_model=None,
+                 pipeline=None, device=None):
+        import torch
+        from .model import build_model
+        from .pipeline import LocalPipeline
+        cfg.validate()
+        self.cfg = cfg
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.target = target_model or build_model(cfg.target_config(), self.device)
+        self.draft_model = None
+        if cfg.uses_draft():
+            self.draft_model = draft_model or build_model(cfg.draft_config(), self.device)
+        ranges = plan_layer_split(self.target.config.n_layers, cfg.n_stages(), cfg.node_weights)
+        self.pipe = pipeline or LocalPipeline(self.target, ranges, partitions=cfg.partitions,
+                                              capacity=cfg.capacity,
+                                              max_tokens=cfg.max_run_tokens)
+        self.draft = None
+        self._draft_stream = torch.cuda.Stream(self.device) if cfg.uses_draft() else None
+        self._tables: Dict[int, tuple] = {}
+
+    def _make_draft(self, prompt: List[int], prompt_seed: int):
+        from .drafting import ModelDraftServer, TableDraftServer
+        cfg = self.cfg
+        if not cfg.uses_draft():
+            return None
+        if cfg.draft_backend == "synthetic":
+            key = hash(tuple(prompt))
+            if key not in self._tables:
+                self._tables[key] = truth_table(self.target, prompt,
+                                                cfg.gen_len + 16)
+            truth, runner = self._tables[key]
+            seed = cfg.draft_seed * 1000003 + prompt_seed
+            return TableDraftServer(self.draft_model, truth, runner, cfg.alpha, seed,
+                                    stream=self._draft_stream,
+                                    capacity=min(cfg.capacity, 16 * cfg.max_context))
+        if self.draft is None:
+            self.draft = ModelDraftServer(self.draft_model, stream=self._draft_stream,
+                                          capacity=min(cfg.capacity, 16 * cfg.max_context))
+        else:
+            self.draft.reset()
+        return self.draft
+
+    def run(self, prompt_seed: Optional[int] = None, prompt: Optional[List[int]] = None,
+            mode: Optional[str] = None) -> SimResult:
+        cfg = self.cfg if mode is None else replace(self.cfg, mode=mode)
+        seed = cfg.prompt_seed if prompt_seed is None else prompt_seed
+        if prompt is None:
+            prompt = sample_prompt(seed, cfg.prompt_len, self.target.config.vocab_size)
+        if mode is not None and cfg.n_stages() != self.pipe.n_stages:
+            raise EngineError("mode override must keep the pipeline depth")
+        self.pipe.reset()
+        draft = self._make_draft(prompt, seed)
+        wall0 = time.perf_counter()
+        head = Head(cfg, self.pipe, draft, prompt, self.target.config.embed_dim)
+        runner = {"iterative": head.run_iterative,
+                  "pipeline-iterative": head.run_iterative,
+                  "sync-speculative": head.run_sync_speculative,
+                  "async-speculative": head.run_async_speculative}[cfg.mode]
+        runner()
+        wall = time.perf_counter() - wall0
+        metrics = head.build_metrics(wall)
+        sent = dict(head.msgs)
+        node_logs = dict(head.stage_logs)
+        if draft is not None:
+            node_logs[cfg.nodes] = [("served", draft.forwards)]
+        return SimResult(tokens=head.accepted[len(prompt):], metrics=metrics,
+                         accepted_full=list(head.accepted),
+                         accept_events=list(head.accept_events),
+                         cancel_log=list(head.cancel_log), node_logs=node_logs,
+                         consumed=dict(sent), sent=sent, records=list(head.records))
+
+    def generate(self, prompt: Sequence[int], gen_len: Optional[int] = None) -> List[int]:
+        """The north star's generate(): accepted tokens after ``prompt``."""
+        if gen_len is not None and gen_len != self.cfg.gen_len:
+            self.cfg = replace(self.cfg, gen_len=gen_len)
+        return self.run(prompt=list(prompt)).tokens
+
+
+_ENGINES: Dict[tuple, Engine] = {}
+
+
+def simulate(cfg: ExperimentConfig, target_model=None, draft_model=None) -> SimResult:
+    """Run one experiment to completion on the GPU (engine.py:1293-1356).
+
+    Engines (models + stages) are cached per model-shaping config so
+    repeated calls with different seeds/modes reuse resident weights.
+    """
+    cfg.validate()
+    key = (cfg.target_config(), cfg.draft_config() if cfg.uses_draft() else None,
+           cfg.n_stages(), cfg.node_weights, cfg.partitions, cfg.capacity,
+           cfg.max_run_tokens, cfg.mode in ("sync-speculative", "async-speculative"),
+           id(target_model), id(draft_model))
+    eng = _ENGINES.get(key)
+    if eng is None:
+        if len(_ENGINES) > 4:
+            _ENGINES.clear()
+        eng = Engine(cfg, target_model, draft_model)
+        _ENGINES[key] = eng
+    eng.cfg = cfg
+    return eng.run()
+
+
+def generate(prompt: Sequence[int], cfg: Optional[ExperimentConfig] = None,
+             **overrides) -> List[int]:
+    """Greedy generation of ``cfg.gen_len`` tokens after ``prompt``."""
+    cfg = replace(cfg or ExperimentConfig(), prompt_len=len(prompt), **overrides)
+    cfg.validate()
+    key = ("gen", cfg.target_config(), cfg.draft_config() if cfg.uses_draft() else None,
+           cfg.n_stages(), cfg.mode)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = Engine(cfg)
+        _ENGINES[key] = eng
+    eng.cfg = cfg
+    return eng.run(prompt=list(prompt)).tokens

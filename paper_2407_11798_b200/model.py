@@ -340,7 +340,7 @@ def build_model(config: ModelConfig, device=None, layer_range=None,
     tdt = torch.float32 if config.weight_dtype == "fp32" else torch.bfloat16
 
     def dev(a):
-        return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=tdt)
+        return torch.from_numpy(np.array(a, copy=True)).to(device=device, dtype=tdt)
 
     if config.arch == "ref":
         host = _ref_host_weights(config)

@@ -1,0 +1,151 @@
+"""Target pipelines: where a launched run's stage evaluations execute.
+
+The head (``engine.Head``) talks to a pipeline through five calls that stand
+in for the reference's transactions (transport.py:234-271, engine.py:749-796):
+
+* ``launch(run_id, kind, toks, flags, rows)`` — RUN_CONFIG + ACTIVATIONS:
+  every stage's evaluation of the run is enqueued at once, in stream order;
+* ``copy(src, dsts, end)`` / ``remove(seq, from)`` — CACHE_COPY / CACHE_REMOVE,
+  enqueued on every stage behind the runs launched before them;
+* ``cancel(run_id)`` — CANCEL: a device-visible word that overtakes queued
+  work because kernels read it when they execute;
+* ``poll()`` / ``wait()`` — LOGITS, strictly FIFO (``cudaEventQuery``
+  replaces ``Network.probe``).
+
+``LocalPipeline`` hosts all stages in this process on one GPU (stages run
+back to back on one stream; used for 1-GPU runs and to exercise multi-stage
+semantics).  ``dist.DistPipeline`` spreads the stages over torchrun ranks.
+"""
+
+from __future__ import annotations
+
+from collections import deque
+from dataclasses import dataclass
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib
+from .model import RowResult
+from .runtime import RES_DTYPE, Stage
+
+RESULT_RING = 64
+
+
+@dataclass
+class RunResult:
+    run_id: int
+    placeholder: bool
+    rows: List[RowResult]
+    err: int
+    stage_status: List[int]
+
+
+class LocalPipeline:
+    def __init__(self, model, ranges, partitions: int = 8, capacity: int = 8192,
+                 max_tokens: int = 256, cancel_size: int = 1024, stream=None,
+                 device=None):
+        import torch
+
+        self.device = model.device if device is None else device
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+        self.cancel = torch.zeros(cancel_size, dtype=torch.int32).pin_memory()
+        self.cancel_np = self.cancel.numpy()
+        self.cancel_size = cancel_size
+        self.stages = [Stage(model, lo, hi, capacity=capacity, max_tokens=max_tokens,
+                             n_seq_ids=partitions, stream=self.stream,
+                             cancel_table=self.cancel.data_ptr(),
+                             cancel_size=cancel_size)
+                       for lo, hi in ranges]
+        S = len(self.stages)
+        self.n_stat = (S + 3) // 4
+        rows = 1 + self.n_stat + max_tokens
+        self.res = torch.zeros((RESULT_RING, rows, 4), dtype=torch.int32, device=self.device)
+        self.res_host = torch.zeros((RESULT_RING, rows, 4), dtype=torch.int32).pin_memory()
+        self.res_np = self.res_host.numpy()
+        self.events = [torch.cuda.Event() for _ in range(RESULT_RING)]
+        self.fifo: deque = deque()
+        self.max_tokens = max_tokens
+
+    @property
+    def n_stages(self) -> int:
+        return len(self.stages)
+
+    def reset(self) -> None:
+        if self.fifo:
+            raise RuntimeError("reset with runs in flight")
+        for st in self.stages:
+            st.reset()
+        self.cancel_np[:] = 0
+        self.stream.synchronize()
+
+    # -- transactions -----------------------------------------------------------
+    def launch(self, run_id: int, kind: int, toks: np.ndarray, flags: int,
+               rows: List[int]) -> None:
+        if len(self.fifo) >= RESULT_RING:
+            raise RuntimeError("too many runs in flight")
+        slot = run_id % RESULT_RING
+        blk = self.res[slot]
+        prev = None
+        for i, st in enumerate(self.stages):
+            stat = blk[1 + i // 4, i % 4:].data_ptr()
+            st.forward(toks, run_id, kind, flags,
+                       x_in=None if prev is None else prev.x.data_ptr(),
+                       in_status=None if prev is None else prev_stat,
+                       x_out=st.x.data_ptr(), out_status=stat)
+            prev, prev_stat = st, stat
+        last = self.stages[-1]
+        nrow = len(rows)
+        if nrow:
+            last.lmhead(rows, out=blk[1 + self.n_stat:].data_ptr(),
+                        err_out=blk[0, 1:].data_ptr())
+        nb = 1 + self.n_stat + nrow
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.res_host[slot, :nb].copy_(blk[:nb], non_blocking=True)
+        ev = self.events[slot]
+        ev.record(self.stream)
+        self.fifo.append((run_id, slot, nrow))
+
+    def copy(self, src: int, dsts, end_pos: int) -> None:
+        for st in self.stages:
+            st.cache_copy(src, dsts, end_pos)
+
+    def remove(self, seq: int, from_pos: int) -> None:
+        for st in self.stages:
+            st.cache_remove(seq, from_pos)
+
+    def cancel_run(self, run_id: int) -> None:
+        # host store into mapped pinned memory: visible to kernels at once
+        self.cancel_np[run_id % self.cancel_size] = run_id
+
+    # -- completions ------------------------------------------------------------
+    def ready(self) -> bool:
+        return bool(self.fifo) and self.events[self.fifo[0][1]].query()
+
+    def _collect(self) -> RunResult:
+        run_id, slot, nrow = self.fifo.popleft()
+        blk = self.res_np[slot]
+        stats = blk[1:1 + self.n_stat].reshape(-1)[:self.n_stages].tolist()
+        placeholder = stats[-1] == _lib.SP_STATUS_PLACEHOLDER
+        err = int(blk[0, 1])
+        rows = []
+        if not placeholder and nrow:
+            rr = blk[1 + self.n_stat:1 + self.n_stat + nrow].view(RES_DTYPE).reshape(-1)
+            rows = [RowResult(r["a"], r["b"], r["c"], r["d"]) for r in rr]
+        return RunResult(run_id, placeholder, rows, err, stats)
+
+    def poll(self) -> Optional[RunResult]:
+        return self._collect() if self.ready() else None
+
+    def wait(self) -> RunResult:
+        if not self.fifo:
+            raise RuntimeError("wait with an empty FIFO")
+        self.events[self.fifo[0][1]].synchronize()
+        return self._collect()
+
+    def in_flight(self) -> int:
+        return len(self.fifo)
+
+    def shutdown(self) -> None:
+        self.stream.synchronize()
