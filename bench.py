@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark: single-request generated tokens/s + ITL of PipeInfer on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One *step* = one complete single-request generation (prefill of a 128-token
+synthetic prompt, then ``gen_len`` accepted tokens) of the Llama-2-7B-shape
+target (bf16, random init) with a 160M-shape draft, i.e. BASELINE.json
+configs[1], in PipeInfer's async-speculative mode over an N-stage pipeline
+(one stage per GPU; N=1 is the single-GPU pipeline).  ``value`` is the
+reference's generation speed (engine.py:1234-1243: accepted tokens after
+prefill / time from end of prefill to the last acceptance), aggregated over
+the K timed steps; ``itl_ms`` the mean inter-token latency.
+
+``--impl reference`` times the reference's CPU algorithm (the float64 oracle
+restatement, oracle/) on this host's cores on a bounded sample of the same
+workload (2 decoder layers at 7B width, extrapolated to 32 layers + head).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TARGET, DRAFT = "llama2-7b", "llama-160m"
+ALPHA = 0.66          # paper's observed acceptance for a 7B pair
+PROMPT_LEN, GEN_LEN, MAX_CTX = 128, 512, 1024
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (float64 oracle) on host cores
+# ---------------------------------------------------------------------------
+
+def cpu_baseline(n_decode: int = 3, layers: int = 2, prompt_len: int = 16) -> dict:
+    import numpy as np
+    from oracle import model as OM
+    from oracle.kvcache import OracleCache
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    d, f, V, H = 4096, 11008, 32000, 32
+    r = np.random.Generator(np.random.PCG64(0))
+    cfg = OM.OracleConfig(vocab_size=V, embed_dim=d, n_layers=layers, n_heads=H,
+                          max_context=1024, arch="llama", ffn_dim=f)
+    lw = []
+    for _ in range(layers):
+        lw.append(dict(wq=r.standard_normal((d, d)) / 64, wk=r.standard_normal((d, d)) / 64,
+                       wv=r.standard_normal((d, d)) / 64, wo=r.standard_normal((d, d)) / 64,
+                       wg=r.standard_normal((d, f)) / 64, wu=r.standard_normal((d, f)) / 64,
+                       wd=r.standard_normal((f, d)) / 105, attn_norm=np.ones(d),
+                       mlp_norm=np.ones(d)))
+    emb = r.standard_normal((V, d))
+    w_out = r.standard_normal((d, V)) / 64
+    m = OM.OracleModel(cfg, emb, None, lw, w_out, np.ones(d))
+    cache = OracleCache(d, range(layers), 1024, 1)
+    prompt = [int(t) for t in r.integers(0, V, prompt_len)]
+    OM.eval_layers(m, 0, layers, None,
+                   [(t, i, frozenset([0]), False) for i, t in enumerate(prompt)], cache)
+    t_layers = []
+    for i in range(n_decode):
+        tok = [(int(r.integers(0, V)), prompt_len + i, frozenset([0]), True)]
+        t0 = time.perf_counter()
+        x = OM.eval_layers(m, 0, layers, None, tok, cache)
+        t_layers.append(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    OM.logits(m, x, tok)
+    t_head = time.perf_counter() - t0
+    per_layer = statistics.median(t_layers) / layers
+    per_token = per_layer * 32 + t_head
+    return {"value": 1.0 / per_token, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": (f"oracle fp64 llama forward, {layers} layers at 7B width "
+                       f"(d=4096, ffn=11008), {n_decode} decode tokens after a "
+                       f"{prompt_len}-token prompt, + LM head V=32000; per-token time "
+                       f"extrapolated to 32 layers ({per_layer*1e3:.1f} ms/layer, "
+                       f"head {t_head*1e3:.1f} ms)"),
+            "ms_per_token": per_token * 1e3}
+
+
+# ---------------------------------------------------------------------------
+# roofline: the dominant kernel (weight-streaming GEMV) timed with CUDA events
+# ---------------------------------------------------------------------------
+
+def gemv_roofline(engine, reps: int = 3) -> dict:
+    """Time the full M=1 GEMV set of one decode token (4 GEMVs x L layers of
+    this rank's stage + LM head if present) with CUDA events on the stage
+    stream.  Algorithmic bytes = weight bytes + activation bytes."""
+    import torch
+    from paper_2407_11798_b200 import _lib
+    from paper_2407_11798_b200.model import TOKEN_DTYPE
+    import ctypes as C
+    import numpy as np
+    st = engine.pipe.stages[0]
+    cfg = st.cfg
+    lib = st.lib
+    d, f = cfg.embed_dim, cfg.hidden
+    q, kv = cfg.n_heads * cfg.head_dim, cfg.kv_dim
+    dev = st.device
+    x = torch.randn((8, max(d, f)), device=dev, dtype=torch.float32)
+    out = torch.zeros((8, 2 * f + q + 2 * kv), device=dev, dtype=torch.float32)
+    toks = torch.zeros(8 * 4, dtype=torch.int32, device=dev)
+    kc = torch.zeros((16, kv), dtype=torch.bfloat16, device=dev)
+    wb = 2
+    launches = []
+    for l in range(st.lo, st.hi):
+        L = engine.target.layers[l]
+        launches.append((L["qkv"], q + 2 * kv, d, _lib.SP_EPI_QKV, 1))
+        launches.append((L["o"], d, q, _lib.SP_EPI_RESID, 0))
+        launches.append((L["up"], 2 * f, d, _lib.SP_EPI_SWIGLU, 1))
+        launches.append((L["down"], d, f, _lib.SP_EPI_RESID, 0))
+    args = []
+    nbytes = 0
+    for w, n, k, epi, norm in launches:
+        a = _lib.sp_gemv_args()
+        a.w, a.w_dtype, a.n_rows, a.k = w.data_ptr(), _lib.SP_DTYPE_BF16, n, k
+        a.x, a.m, a.ldx = x.data_ptr(), 1, x.shape[1]
+        a.norm, a.norm_eps, a.gain = norm, 1e-5, None
+        a.epi, a.out, a.ldo = epi, out.data_ptr(), out.shape[1]
+        a.q_rows, a.kv_rows, a.k_cache, a.v_cache = q, kv, kc.data_ptr(), kc.data_ptr()
+        a.cache_row0, a.rope, a.head_dim, a.rope_theta = 0, 1, cfg.head_dim, 10000.0
+        a.toks, a.err, a.run_state = toks.data_ptr(), None, None
+        args.append(a)
+        nbytes += n * k * wb + 4 * (k + n)
+    s = st.stream
+    times = []
+    for rep in range(reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for a in args:
+            _lib.check(lib.sp_gemv(C.byref(a), s.cuda_stream))
+        e1.record(s)
+        e1.synchronize()
+        if rep:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t = min(times)
+    peak, how = _peaks()
+    achieved = nbytes / t / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_gemv_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get("bytes_per_launch")
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": "gemv_kernel<bf16,MT=1> (QKV+O+gate/up+down of every layer of the "
+                      "stage, one decode token)",
+            "algorithmic_bytes_per_launch": round(nbytes / len(args)),
+            "avg_launch_us": round(t / len(args) * 1e6, 2), "launches": len(args),
+            "peak_source": how}
+
+
+# ---------------------------------------------------------------------------
+
+def run_ours(args) -> dict:
+    import torch
+    import paper_2407_11798_b200 as sp
+    from paper_2407_11798_b200.engine import Engine, ExperimentConfig
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        from paper_2407_11798_b200 import dist
+        return dist.bench_main(args)
+    torch.cuda.set_device(0)
+    cfg = ExperimentConfig(mode="async-speculative", nodes=2, target_shape=TARGET,
+                           draft_shape=DRAFT, draft_backend="synthetic", alpha=ALPHA,
+                           prompt_len=PROMPT_LEN, gen_len=args.gen_len, max_context=MAX_CTX,
+                           target_seed=1, draft_seed=2, capacity=8192)
+    eng = Engine(cfg)
+    seeds = [1234 + i for i in range(args.warmup + args.steps)]
+    for s in seeds:   # synthetic-draft truth tables: setup, outside the timed region
+        eng._make_draft(sp.sample_prompt(s, PROMPT_LEN, 32000), s)
+    for i in range(args.warmup):
+        eng.run(prompt_seed=seeds[i])
+    torch.cuda.synchronize()
+    res = []
+    launches0 = eng.launch_count() if hasattr(eng, "launch_count") else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(0) as clk:
+        e0.record()
+        for i in range(args.steps):
+            res.append(eng.run(prompt_seed=seeds[args.warmup + i]))
+        e1.record()
+        torch.cuda.synchronize()
+    total_s = e0.elapsed_time(e1) / 1e3
+    gen_tok = sum(r.metrics.tokens_generated - 1 for r in res)
+    gen_time = sum(r.metrics.duration for r in res)
+    value = gen_tok / gen_time
+    itl = statistics.mean(r.metrics.itl for r in res)
+    launches = (eng.launch_count() - launches0) if launches0 is not None else None
+    # sync-speculative on the same kernels (the >=2x target's denominator)
+    sync = [eng.run(prompt_seed=seeds[args.warmup + i], mode="sync-speculative")
+            for i in range(min(2, args.steps))]
+    it = [eng.run(prompt_seed=seeds[args.warmup], mode="iterative")] if False else []
+    sync_speed = (sum(r.metrics.tokens_generated - 1 for r in sync) /
+                  sum(r.metrics.duration for r in sync))
+    # e2e: the public API with host buffers (prompt H2D, tokens D2H inside)
+    prompt = sp.sample_prompt(seeds[-1], PROMPT_LEN, 32000)
+    t0 = time.perf_counter()
+    out = eng.generate(prompt)
+    e2e_s = time.perf_counter() - t0
+    rf = gemv_roofline(eng)
+    cpu = cpu_baseline() if not args.no_cpu else None
+    line = {
+        "metric": "single-request generated tokens/s + inter-token latency",
+        "value": round(value, 2), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_s / args.steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (random-init weights, PCG64 prompts)",
+        "config": {"workload": "configs[1]: Llama-2-7B-shape target + 160M-shape draft, "
+                               "bf16, async-speculative (PipeInfer), 1 pipeline stage",
+                   "target": TARGET, "draft": DRAFT, "alpha": ALPHA,
+                   "prompt_len": PROMPT_LEN, "gen_len": args.gen_len,
+                   "pipeline_stages": 1, "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
+        "itl_ms": round(itl * 1e3, 3),
+        "acceptance_rate": round(statistics.mean(r.metrics.acceptance_rate for r in res), 4),
+        "sync_speculative_tokens_per_s": round(sync_speed, 2),
+        "async_over_sync": round(value / sync_speed, 3),
+        "weight_stream_roofline_tokens_per_s": round(rf["peak"] * 1e9 / eng.target.config.weight_bytes(), 1),
+        "e2e": {"value": round((len(out) - 1) / e2e_s, 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": PROMPT_LEN * 16, "d2h_bytes_per_step": len(out) * 16,
+                "note": "generate() on host token lists, prefill included"},
+        "gpu_launches": launches,
+        "roofline": rf,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    return line
+
+
+def run_reference(args) -> dict:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(n_decode=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(n_decode=2))
+    el = time.perf_counter() - t0
+    v = statistics.median(x["value"] for x in vals)
+    c = vals[0]
+    return {"metric": "single-request generated tokens/s + inter-token latency",
+            "value": round(v, 4), "unit": "tokens/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (random-init weights)", "impl": "reference",
+            "config": {"workload": "configs[1]: Llama-2-7B-shape target (CPU reference "
+                                   "algorithm, float64, one request)",
+                       "target": TARGET, "prompt_len": PROMPT_LEN},
+            "itl_ms": round(1e3 / v, 1),
+            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": c["cores"],
+                             "kind": "port", "sample": c["sample"]},
+            "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--gen-len", type=int, default=GEN_LEN)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None and int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -33,21 +33,27 @@ from .runtime import RES_DTYPE, Stage
 
 class _DraftBase:
     def __init__(self, draft_model, stream=None, capacity: Optional[int] = None,
-                 max_tokens: int = 256):
+                 max_tokens: int = 256, stage: Optional[Stage] = None):
         import torch
         self.model = draft_model
         cfg = draft_model.config
         self.max_context = cfg.max_context
-        self.stream = stream if stream is not None else torch.cuda.Stream(draft_model.device)
-        cap = capacity or max(1024, 8 * cfg.max_context)
-        self.stage = Stage(draft_model, 0, cfg.n_layers, capacity=cap,
-                           max_tokens=max_tokens, n_seq_ids=1, stream=self.stream)
+        if stage is not None:          # reuse a resident stage (cleared)
+            self.stream = stage.stream
+            self.stage = stage
+            stage.reset()
+        else:
+            self.stream = stream if stream is not None else torch.cuda.Stream(draft_model.device)
+            cap = capacity or max(1024, 8 * cfg.max_context)
+            self.stage = Stage(draft_model, 0, cfg.n_layers, capacity=cap,
+                               max_tokens=max_tokens, n_seq_ids=1, stream=self.stream)
         self.res = torch.zeros((8, 4), dtype=torch.int32, device=draft_model.device)
         self.res_host = torch.zeros((8, 4), dtype=torch.int32).pin_memory()
         self.event = torch.cuda.Event()
         self.tokens: List[int] = []
         self._pending = None
         self.forwards = 0          # draft-model forwards issued (cost accounting)
+        torch.cuda.synchronize(draft_model.device)
 
     def __len__(self) -> int:
         return len(self.tokens)
@@ -150,8 +156,8 @@ class TableDraftServer(_DraftBase):
 
     def __init__(self, draft_model, truth: Sequence[int], runner: Sequence[int],
                  alpha: float, seed: int, stream=None, capacity=None,
-                 charge: bool = True, max_tokens: int = 256):
-        super().__init__(draft_model, stream, capacity, max_tokens)
+                 charge: bool = True, max_tokens: int = 256, stage=None):
+        super().__init__(draft_model, stream, capacity, max_tokens, stage)
         if not 0.0 <= alpha <= 1.0:
             raise SpeculationError(f"alpha must be in [0,1], got {alpha}")
         self.alpha = float(alpha)

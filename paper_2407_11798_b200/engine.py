@@ -855,9 +855,15 @@ class Engine:
                                                 cfg.gen_len + 16)
             truth, runner = self._tables[key]
             seed = cfg.draft_seed * 1000003 + prompt_seed
-            return TableDraftServer(self.draft_model, truth, runner, cfg.alpha, seed,
-                                    stream=self._draft_stream,
-                                    capacity=min(cfg.capacity, 16 * cfg.max_context))
+            prev = getattr(self, "_table_draft", None)
+            srv = TableDraftServer(self.draft_model, truth, runner, cfg.alpha, seed,
+                                   stream=self._draft_stream,
+                                   capacity=min(cfg.capacity, 16 * cfg.max_context),
+                                   stage=None if prev is None else prev.stage)
+            if prev is not None:
+                srv.forwards = 0
+            self._table_draft = srv
+            return srv
         if self.draft is None:
             self.draft = ModelDraftServer(self.draft_model, stream=self._draft_stream,
                                           capacity=min(cfg.capacity, 16 * cfg.max_context))
@@ -893,6 +899,14 @@ class Engine:
                          accept_events=list(head.accept_events),
                          cancel_log=list(head.cancel_log), node_logs=node_logs,
                          consumed=dict(sent), sent=sent, records=list(head.records))
+
+    def launch_count(self) -> int:
+        """Kernels this process has launched through the C ABI so far."""
+        n = sum(st.launches for st in getattr(self.pipe, "stages", []))
+        for d in (self.draft, getattr(self, "_table_draft", None)):
+            if d is not None:
+                n += d.stage.launches
+        return n
 
     def generate(self, prompt: Sequence[int], gen_len: Optional[int] = None) -> List[int]:
         """The north star's generate(): accepted tokens after ``prompt``."""

@@ -340,14 +340,18 @@ def build_model(config: ModelConfig, device=None, layer_range=None,
     tdt = torch.float32 if config.weight_dtype == "fp32" else torch.bfloat16
 
     def dev(a):
-        return torch.from_numpy(np.array(a, copy=True)).to(device=device, dtype=tdt)
+        # order="C": the kernels stream [d_out, d_in] rows; a transposed
+        # (F-ordered) host array must be physically re-laid out
+        return torch.from_numpy(np.array(a, order="C", copy=True)).to(
+            device=device, dtype=tdt).contiguous()
 
     if config.arch == "ref":
         host = _ref_host_weights(config)
         m.host = host
         if want_emb:
             m.embedding = dev(host["embedding"])
-            m.pos_table = torch.from_numpy(host["pos_table"]).to(device, torch.float32)
+            m.pos_table = torch.from_numpy(np.array(host["pos_table"], order="C")).to(
+                device, torch.float32).contiguous()
         for l in range(lo, hi):
             lw = host["layers"][l]
             m.layers[l] = dict(

@@ -64,6 +64,7 @@ class LocalPipeline:
         self.res_host = torch.zeros((RESULT_RING, rows, 4), dtype=torch.int32).pin_memory()
         self.res_np = self.res_host.numpy()
         self.events = [torch.cuda.Event() for _ in range(RESULT_RING)]
+        torch.cuda.synchronize(self.device)
         self.fifo: deque = deque()
         self.max_tokens = max_tokens
 

@@ -22,7 +22,11 @@ RES_DTYPE = np.dtype([("a", "<i4"), ("b", "<i4"), ("c", "<f4"), ("d", "<f4")])
 
 
 def _ptr(t) -> Optional[int]:
-    return None if t is None else t.data_ptr()
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ModelError("device weights must be contiguous (row-major [d_out, d_in])")
+    return t.data_ptr()
 
 
 class Stage:
@@ -72,7 +76,10 @@ class Stage:
         self.logits_dev = None
         self._last_batch = None
         self._last_hi = None
-        self._run_counter = 0
+        self.launches = 0
+        # buffers were zero-filled on the creating stream: order them before
+        # any kernel on self.stream can touch them
+        torch.cuda.synchronize(self.device)
 
     def __del__(self):
         try:
@@ -106,6 +113,8 @@ class Stage:
             x_out if x_out is not None else self.x.data_ptr(), out_status,
             1 if chain else 0, layer_a, layer_b, self.s)
         check(rc, "sp_stage_forward")
+        nl = (self.hi - self.lo) if layer_a < 0 else (layer_b - layer_a)
+        self.launches += 5 * nl + (2 if flags & _lib.SP_FWD_CONTINUE else 4)
 
     def lmhead(self, rows: Sequence[int], x: Optional[int] = None,
                out: Optional[int] = None, logits: Optional[int] = None,
@@ -118,6 +127,7 @@ class Stage:
             err_out if err_out is not None else self.res[0, 1:].data_ptr(),
             1 if update_tip else 0, 1 if chain_gate else 0, float(cutoff), self.s)
         check(rc, "sp_stage_lmhead")
+        self.launches += 2
 
     def cache_copy(self, src: int, dsts, end_pos: int) -> None:
         mask = 0
@@ -127,10 +137,12 @@ class Stage:
             mask |= 1 << int(dd)
         check(self.lib.sp_stage_cache_copy(self.h, int(src), mask, int(end_pos), self.s),
               "cache_copy")
+        self.launches += 1
 
     def cache_remove(self, seq: int, from_pos: int) -> None:
         check(self.lib.sp_stage_cache_remove(self.h, int(seq), int(from_pos), self.s),
               "cache_remove")
+        self.launches += 1
 
     def cache_keep(self, seq: int) -> None:
         check(self.lib.sp_stage_cache_keep(self.h, int(seq), self.s), "cache_keep")

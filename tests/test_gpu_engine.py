@@ -1,0 +1,185 @@
+"""GPU engine: every decoding mode reproduces the reference's serial greedy
+stream (tests/test_engine.py + criterion 1/2 of test_acceptance.py, re-pointed
+at the B200 pipeline), with the reference's invariants on cancellation,
+FIFO completion and partition exhaustion."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sp():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2407_11798_b200 as sp
+    return sp
+
+
+BASE = dict(mode="async-speculative", nodes=4, vocab_size=64, embed_dim=32,
+            target_layers=6, draft_layers=2, max_context=512, prompt_len=16,
+            gen_len=20, prompt_seed=5, target_seed=7, draft_seed=11,
+            cutoff=0.0, cutoff_decay=0.0)
+
+
+def cfg(sp, **kw):
+    return sp.ExperimentConfig(**{**BASE, **kw})
+
+
+# Speculation only pays when a draft request is cheaper than a target run.
+# The reference's tests get that from their simulated delays; on the GPU
+# tiny models are launch-bound, so these tests use a deep target and a
+# one-layer draft to make the draft genuinely faster.
+DEEP = dict(target_layers=24, draft_layers=1)
+
+
+def deep(sp, **kw):
+    return cfg(sp, **{**DEEP, **kw})
+
+
+def _golden_stream(golden, seed):
+    for e in golden["engine"]:
+        if e["mode"] == "iterative" and e["prompt_seed"] == seed:
+            return e["tokens"]
+    raise KeyError(seed)
+
+
+@pytest.mark.parametrize("seed", [5, 21])
+def test_all_modes_byte_identical(sp, golden, seed):
+    want = _golden_stream(golden, seed)
+    for mode, nodes in [("iterative", 1), ("pipeline-iterative", 3),
+                        ("sync-speculative", 4), ("async-speculative", 4)]:
+        res = sp.simulate(cfg(sp, mode=mode, nodes=nodes, prompt_seed=seed))
+        assert res.tokens == want, f"{mode} diverged"
+        assert res.metrics.token_checksum == sp.token_checksum(want)
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.35, 0.8, 1.0])
+def test_synthetic_alpha_equivalence(sp, golden, alpha):
+    res = sp.simulate(cfg(sp, draft_backend="synthetic", alpha=alpha))
+    assert res.tokens == _golden_stream(golden, 5)
+
+
+def test_weighted_pipeline_equivalence(sp, golden):
+    res = sp.simulate(cfg(sp, mode="pipeline-iterative", nodes=3, node_weights=(2, 1, 3)))
+    assert res.tokens == _golden_stream(golden, 5)
+
+
+def test_alpha_one_no_rejections(sp):
+    m = sp.simulate(deep(sp, draft_backend="synthetic", alpha=1.0, gen_len=48)).metrics
+    assert m.examined > 0
+    assert m.matched == m.examined
+    assert m.acceptance_rate == 1.0
+    assert m.cancelled_runs == 0
+
+
+def test_alpha_zero_equals_iterative(sp):
+    res = sp.simulate(cfg(sp, draft_backend="synthetic", alpha=0.0, gen_len=16))
+    it = sp.simulate(cfg(sp, mode="iterative", nodes=1, gen_len=16))
+    assert res.tokens == it.tokens
+    assert res.metrics.matched == 0
+
+
+def test_cancelled_runs_provably_stale(sp):
+    res = sp.simulate(deep(sp, draft_backend="synthetic", alpha=0.4, gen_len=64))
+    assert res.cancel_log, "expected cancellations at alpha=0.4"
+    truth = res.accepted_full
+    for e in res.cancel_log:
+        if e.reason == "superfluous":
+            assert e.max_pos < e.accepted_len_at_cancel - 1
+        else:
+            assert [p for p, t in e.chain
+                    if p < e.accepted_len_at_cancel and t != truth[p]], e
+
+
+def test_pipeline_integrity(sp):
+    res = sp.simulate(deep(sp, draft_backend="synthetic", alpha=0.5, gen_len=32))
+    assert all(r.status != "in-flight" for r in res.records)
+    times = [t for t, _ in res.accept_events]
+    assert times == sorted(times)
+    assert res.metrics.msgs_by_tag["LOGITS"] == res.metrics.runs_started
+    kinds = {"run-config", "cache-copy", "cache-remove"}
+    proj = [[e for e in res.node_logs[s] if e[0] in kinds] for s in (1, 2, 3)]
+    assert proj[0] == proj[1] == proj[2]
+
+
+def test_partition_exhaustion_stalls_not_crashes(sp, golden):
+    res = sp.simulate(deep(sp, draft_backend="synthetic", alpha=1.0, partitions=2,
+                           gen_len=16))
+    assert res.tokens == sp.simulate(deep(sp, mode="iterative", nodes=1, gen_len=16)).tokens
+    assert res.metrics.spec_runs > 0
+
+
+def test_eos_halts(sp):
+    probe = sp.simulate(cfg(sp, mode="iterative", nodes=1, gen_len=12))
+    eos = probe.tokens[4]
+    res = sp.simulate(cfg(sp, mode="iterative", nodes=1, gen_len=12, eos_token=eos))
+    assert res.tokens == probe.tokens[:5]
+    res = sp.simulate(cfg(sp, gen_len=12, eos_token=probe.tokens[5]))
+    idx = res.tokens.index(probe.tokens[5])
+    assert res.tokens == probe.tokens[:idx + 1]
+
+
+def test_metric_identity(sp):
+    m = sp.simulate(deep(sp, draft_backend="synthetic", alpha=0.7, gen_len=24)).metrics
+    k = m.tokens_generated - 1
+    assert k / (m.ttft + m.itl * (k - 1)) == pytest.approx(m.generation_speed, rel=1e-9)
+
+
+def test_criterion1_cfg1_streams(sp, golden):
+    """256 generated tokens on the reference's criterion-1 model, 4 modes."""
+    for s in golden["streams"][:3]:
+        c = s["config"]
+        for mode, nodes in [("iterative", 1), ("pipeline-iterative", 4),
+                            ("sync-speculative", 5), ("async-speculative", 5)]:
+            res = sp.simulate(sp.ExperimentConfig(
+                mode=mode, nodes=nodes, vocab_size=c["vocab_size"],
+                embed_dim=c["embed_dim"], target_layers=c["n_layers"],
+                n_heads=c["n_heads"], draft_layers=2, max_context=c["max_context"],
+                prompt_len=128, gen_len=256, target_seed=c["seed"], draft_seed=2,
+                prompt_seed=s["prompt_seed"], cutoff=0.0, cutoff_decay=0.0))
+            assert res.tokens == s["tokens"], (mode, s["prompt_seed"])
+
+
+def test_randomized_stress_matches_serial(sp):
+    """Criterion-2 style: randomized speculation settings never change output."""
+    r = np.random.Generator(np.random.PCG64(99))
+    for i in range(24):
+        seed = int(r.integers(0, 4))
+        c = sp.ExperimentConfig(
+            mode="async-speculative", nodes=int(r.integers(2, 6)), vocab_size=16,
+            embed_dim=16, target_layers=4, draft_layers=1, draft_embed_dim=16,
+            max_context=128, prompt_len=8, gen_len=int(r.integers(8, 33)),
+            target_seed=3, prompt_seed=seed,
+            draft_backend=["toy", "synthetic"][int(r.integers(0, 2))],
+            alpha=float(r.choice([0.0, 0.3, 0.6, 0.9, 1.0])),
+            microbatch=int(r.integers(1, 5)), partitions=int(r.integers(2, 9)),
+            continuous=bool(r.integers(0, 2)), cutoff=float(r.choice([0.0, 0.2, 0.5])),
+            cutoff_recovery=float(r.choice([0.0, 0.05])),
+            cutoff_decay=float(r.choice([0.0, 0.05])))
+        res = sp.simulate(c)
+        ref = sp.reference_decode(c.target_config(),
+                                  sp.sample_prompt(seed, 8, 16), c.gen_len)
+        assert res.tokens == ref, c
+
+
+def test_device_draft_loop_matches_host_speculation(sp):
+    """The device-side speculate_microbatch loop (gate words in HBM) proposes
+    exactly what the host loop over the same GPU draft proposes."""
+    from paper_2407_11798_b200.drafting import ModelDraftServer
+    cfgm = sp.ModelConfig(64, 32, 2, 4, 256, 11)
+    dm = sp.build_model(cfgm)
+    srv = ModelDraftServer(dm)
+    host = sp.ToyDraft(dm)
+    prompt = sp.sample_prompt(5, 16, 64)
+    srv.request(0, prompt, 0, 1.0)
+    assert srv.reply() == ((), ())
+    host.feed(prompt)
+    for cut in (0.0, 0.05, 0.1, 0.2, 0.0):
+        srv.request(len(srv), (), 4, cut)
+        toks, confs = srv.reply()
+        st = sp.SpeculationState(host, sp.CutoffController(base=cut, recovery=0, decay=0), 1)
+        props = sp.speculate_microbatch(st, max_tokens=4)
+        assert list(toks) == [t for t, _ in props]
+        assert np.allclose(confs, [c for _, c in props], rtol=1e-6)
