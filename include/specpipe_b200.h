@@ -140,6 +140,13 @@ typedef struct sp_gemv_args {
   const sp_token* toks;   /* positions for RoPE                          */
   int* err;
   const int* run_state;   /* non-zero => skip (cancelled / placeholder)  */
+  /* early inference cancellation (K14): CTA 0 reads *cancel_word and, if it
+   * names run_id, sets *run_state_w so every LATER kernel of the run skips.
+   * Only kernels without cross-CTA state may observe it (a mid-kernel flip
+   * must not strand split-merge tickets). */
+  int* run_state_w;
+  const int* cancel_word;
+  int32_t run_id;
 } sp_gemv_args;
 
 int sp_gemv(const sp_gemv_args* a, void* stream);

@@ -57,7 +57,9 @@ class sp_gemv_args(C.Structure):
                 ("k_cache", C.c_void_p), ("v_cache", C.c_void_p),
                 ("cache_row0", C.c_int32), ("rope", C.c_int32),
                 ("head_dim", C.c_int32), ("rope_theta", C.c_float),
-                ("toks", C.c_void_p), ("err", C.c_void_p), ("run_state", C.c_void_p)]
+                ("toks", C.c_void_p), ("err", C.c_void_p), ("run_state", C.c_void_p),
+                ("run_state_w", C.c_void_p), ("cancel_word", C.c_void_p),
+                ("run_id", C.c_int32)]
 
 
 P = C.c_void_p

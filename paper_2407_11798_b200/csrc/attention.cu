@@ -22,8 +22,11 @@ plan_kernel(const int32_t* __restrict__ cell_pos,
             const uint32_t* __restrict__ cell_mask, int n_old, int row0,
             const sp_token* __restrict__ toks, int n, int max_context,
             int32_t* __restrict__ vis, int32_t* __restrict__ vis_len,
-            int ld_vis, int check_cov, int* err) {
+            int ld_vis, int check_cov, int* err, const int* run_state) {
   extern __shared__ int cnt[];  // [max_context + 1]
+  // a run skipped by its gate is never checked (engine.py:581-590: the
+  // coverage check follows the cancellation test)
+  if (run_skipped(run_state)) return;
   __shared__ int wsum[PLAN_THREADS / 32];
   const int i = blockIdx.x;
   const int tid = threadIdx.x;
@@ -284,7 +287,8 @@ static cudaError_t attn_dispatch(const AttnArgs& a, int hd, cudaStream_t st) {
 cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
                         int n_old, int row0, const sp_token* toks, int n,
                         int max_context, int32_t* vis, int32_t* vis_len,
-                        int ld_vis, int check_cov, int* err, cudaStream_t st) {
+                        int ld_vis, int check_cov, int* err, cudaStream_t st,
+                        const int* run_state) {
   const size_t smem = (size_t)(max_context + 1) * sizeof(int);
   static int configured = 0;
   if (smem > 48 * 1024 && configured < (int)smem) {
@@ -294,7 +298,7 @@ cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
   }
   plan_kernel<<<n, PLAN_THREADS, smem, st>>>(cell_pos, cell_mask, n_old, row0,
                                              toks, n, max_context, vis, vis_len,
-                                             ld_vis, check_cov, err);
+                                             ld_vis, check_cov, err, run_state);
   return cudaGetLastError();
 }
 

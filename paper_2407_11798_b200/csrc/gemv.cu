@@ -15,6 +15,9 @@ template <typename T, int MT, int ROWS, int EPI, bool NORM>
 __global__ void __launch_bounds__(GEMV_THREADS)
 gemv_kernel(const sp_gemv_args a) {
   __shared__ GemvSmem<T, MT, ROWS, NORM> sm;
+  if (a.cancel_word != nullptr && blockIdx.x == 0 && threadIdx.x == 0 &&
+      ld_volatile(a.cancel_word) == a.run_id)
+    atomicExch(a.run_state_w, 1);  // observed once per layer (O projection)
   if (run_skipped(a.run_state)) return;
   const int row0 = blockIdx.x * ROWS;
   const T* W = reinterpret_cast<const T*>(a.w);

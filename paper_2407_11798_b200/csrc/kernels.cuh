@@ -52,7 +52,8 @@ struct LmArgs {
 cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
                         int n_old, int row0, const sp_token* toks, int n,
                         int max_context, int32_t* vis, int32_t* vis_len,
-                        int ld_vis, int check_cov, int* err, cudaStream_t st);
+                        int ld_vis, int check_cov, int* err, cudaStream_t st,
+                        const int* run_state = nullptr);
 cudaError_t launch_attention(const AttnArgs& a, int kv_dtype, int hd,
                              cudaStream_t st);
 int attn_splits(int max_len);

@@ -398,7 +398,7 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
   if (!cont)
     SP_CHECK(launch_plan(s->cell_pos, s->cell_mask, n_old, row0, dd, n,
                          D.max_context, s->vis, s->vis_len, s->ld_vis, check,
-                         s->err, st));
+                         s->err, st, s->run_state));
   // launch bound on visible entries per query (+ self): chain batches see
   // exactly pos cells; otherwise bounded by the table size
   const int bound = check ? (max_pos + 1) : (n_old + n);
@@ -441,15 +441,17 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
     a.nsplit = nsplit; a.scale = 1.0f / sqrtf((float)D.head_dim);
     a.out = s->attn; a.scratch = s->att_scratch; a.tickets = s->att_tickets;
     a.run_state = s->run_state; a.run_state_w = s->run_state;
-    a.cancel_word = cancel_word; a.run_id = run_id; a.err = s->err;
+    a.cancel_word = nullptr; a.run_id = run_id; a.err = s->err;  // see O-proj
     SP_CHECK(launch_attention(a, D.w_dtype, D.head_dim, st));
     // x += attn @ Wo (model.py:416)
     g = sp_gemv_args{};
     g.w_dtype = D.w_dtype; g.run_state = s->run_state; g.err = s->err; g.toks = dd;
     g.m = n; g.w = L.o; g.n_rows = d; g.k = s->q_dim; g.x = s->attn; g.ldx = s->q_dim;
     g.norm = 0; g.epi = SP_EPI_RESID; g.out = x_out; g.ldo = d;
+    g.cancel_word = cancel_word; g.run_state_w = s->run_state; g.run_id = run_id;
     rc = sp_gemv(&g, stream);
     if (rc) return rc;
+    g.cancel_word = nullptr; g.run_state_w = nullptr;
     // h = act(rmsnorm(x) @ W1) (model.py:417-418)
     g.w = L.up; g.n_rows = s->up_rows; g.k = d; g.x = x_out; g.ldx = d;
     g.norm = 1; g.norm_eps = D.norm_eps; g.gain = llama ? L.mlp_norm : nullptr;

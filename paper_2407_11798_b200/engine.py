@@ -723,7 +723,8 @@ class Head:
             self.pending_tip_seq = 0
 
     def _cancel_stale(self) -> None:
-        for rec, reason in detect_stale_runs(self.fifo, self.accepted):
+        stale = detect_stale_runs(self.fifo, self.accepted)
+        for rec, reason in stale:
             rec.status = CANCELLED_INVALID if reason == INVALID else CANCELLED_SUPERFLUOUS
             self._judge_cancelled(rec)
             if reason == INVALID:
@@ -733,12 +734,17 @@ class Head:
             self.cancel_log.append(CancelLogEntry(
                 rec.run_id, reason, rec.kind, rec.min_pos, rec.max_pos,
                 len(self.accepted), tuple(rec.chain())))
-            self.pipe.cancel_run(rec.run_id)
             self._count("CANCEL", (24 + 16) * self.pipe.n_stages, 1, self.pipe.n_stages)
+        # Publish newest first: the device reads these words while it runs,
+        # so a stage that sees an older run cancelled must also see every
+        # later one (a descendant built on a skipped partition is doomed too;
+        # the reference delivers them together, engine.py:1180-1182).
+        for rec, _ in reversed(stale):
+            self.pipe.cancel_run(rec.run_id)
 
     # -- shutdown ------------------------------------------------------------------
     def _finish(self) -> None:
-        for rec in self.fifo:
+        for rec in reversed(self.fifo):
             if rec.status == IN_FLIGHT:
                 rec.status = DRAINED
                 self.drained_runs += 1

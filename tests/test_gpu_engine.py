@@ -84,6 +84,8 @@ def test_alpha_zero_equals_iterative(sp):
 def test_cancelled_runs_provably_stale(sp):
     res = sp.simulate(deep(sp, draft_backend="synthetic", alpha=0.4, gen_len=64))
     assert res.cancel_log, "expected cancellations at alpha=0.4"
+    # early cancellation (skip / mid-stage abandon) never perturbs later runs
+    assert res.tokens == sp.simulate(deep(sp, mode="iterative", nodes=1, gen_len=64)).tokens
     truth = res.accepted_full
     for e in res.cancel_log:
         if e.reason == "superfluous":
