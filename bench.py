@@ -223,12 +223,9 @@ def gemv_roofline(engine, reps: int = 3) -> dict:
 
 def run_ours(args) -> dict:
     import torch
-    import paper_2407_11798_b200 as sp
     from paper_2407_11798_b200.engine import Engine, ExperimentConfig
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if world > 1:
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         from paper_2407_11798_b200 import dist
         return dist.bench_main(args)
     torch.cuda.set_device(0)
@@ -236,7 +233,14 @@ def run_ours(args) -> dict:
                            draft_shape=DRAFT, draft_backend="synthetic", alpha=ALPHA,
                            prompt_len=PROMPT_LEN, gen_len=args.gen_len, max_context=MAX_CTX,
                            target_seed=1, draft_seed=2, capacity=8192)
-    eng = Engine(cfg)
+    return measure(Engine(cfg), args, n_gpus=1)
+
+
+def measure(eng, args, n_gpus: int, pipe=None) -> dict:
+    """The timed protocol, shared by the 1-GPU and torchrun paths (rank 0)."""
+    import torch
+    import paper_2407_11798_b200 as sp
+
     seeds = [1234 + i for i in range(args.warmup + args.steps)]
     for s in seeds:   # synthetic-draft truth tables: setup, outside the timed region
         eng._make_draft(sp.sample_prompt(s, PROMPT_LEN, 32000), s)
@@ -244,59 +248,72 @@ def run_ours(args) -> dict:
         eng.run(prompt_seed=seeds[i])
     torch.cuda.synchronize()
     res = []
-    launches0 = eng.launch_count() if hasattr(eng, "launch_count") else None
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(0) as clk:
-        e0.record()
+    launches0 = eng.launch_count()
+    with Clocks(torch.cuda.current_device()) as clk:
+        if pipe is not None:
+            pipe.mark(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         for i in range(args.steps):
             res.append(eng.run(prompt_seed=seeds[args.warmup + i]))
-        e1.record()
         torch.cuda.synchronize()
-    total_s = e0.elapsed_time(e1) / 1e3
+        total_s = time.perf_counter() - t0
+        if pipe is not None:
+            pipe.mark(2)
+    launches = eng.launch_count() - launches0
     gen_tok = sum(r.metrics.tokens_generated - 1 for r in res)
     gen_time = sum(r.metrics.duration for r in res)
     value = gen_tok / gen_time
     itl = statistics.mean(r.metrics.itl for r in res)
-    launches = (eng.launch_count() - launches0) if launches0 is not None else None
-    # sync-speculative on the same kernels (the >=2x target's denominator)
+    # baselines on the same kernels and pipeline: sync-speculative (the >=2x
+    # target's denominator) and plain pipeline-iterative decoding
+    nb = min(2, args.steps)
     sync = [eng.run(prompt_seed=seeds[args.warmup + i], mode="sync-speculative")
-            for i in range(min(2, args.steps))]
-    it = [eng.run(prompt_seed=seeds[args.warmup], mode="iterative")] if False else []
-    sync_speed = (sum(r.metrics.tokens_generated - 1 for r in sync) /
-                  sum(r.metrics.duration for r in sync))
-    # e2e: the public API with host buffers (prompt H2D, tokens D2H inside)
+            for i in range(nb)]
+    itr = [eng.run(prompt_seed=seeds[args.warmup + i], mode="pipeline-iterative")
+           for i in range(nb)]
+
+    def speed(rs):
+        return sum(r.metrics.tokens_generated - 1 for r in rs) / sum(r.metrics.duration for r in rs)
+
+    sync_speed, it_speed = speed(sync), speed(itr)
+    # e2e: the public API on host token lists (prompt H2D, results D2H inside)
     prompt = sp.sample_prompt(seeds[-1], PROMPT_LEN, 32000)
+    eng._make_draft(prompt, 1234)
     t0 = time.perf_counter()
     out = eng.generate(prompt)
     e2e_s = time.perf_counter() - t0
     rf = gemv_roofline(eng)
     cpu = cpu_baseline() if not args.no_cpu else None
-    line = {
+    wb = eng.target.config.weight_bytes()
+    return {
         "metric": "single-request generated tokens/s + inter-token latency",
-        "value": round(value, 2), "unit": "tokens/s", "n_gpus": 1,
+        "value": round(value, 2), "unit": "tokens/s", "n_gpus": n_gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_s / args.steps * 1e3, 2),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, PCG64 prompts)",
         "config": {"workload": "configs[1]: Llama-2-7B-shape target + 160M-shape draft, "
-                               "bf16, async-speculative (PipeInfer), 1 pipeline stage",
+                               f"bf16, async-speculative (PipeInfer), {n_gpus}-stage pipeline",
                    "target": TARGET, "draft": DRAFT, "alpha": ALPHA,
                    "prompt_len": PROMPT_LEN, "gen_len": args.gen_len,
-                   "pipeline_stages": 1, "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
+                   "pipeline_stages": n_gpus,
+                   "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
         "itl_ms": round(itl * 1e3, 3),
         "acceptance_rate": round(statistics.mean(r.metrics.acceptance_rate for r in res), 4),
+        "cancelled_runs_per_step": round(statistics.mean(r.metrics.cancelled_runs for r in res), 1),
         "sync_speculative_tokens_per_s": round(sync_speed, 2),
+        "pipeline_iterative_tokens_per_s": round(it_speed, 2),
         "async_over_sync": round(value / sync_speed, 3),
-        "weight_stream_roofline_tokens_per_s": round(rf["peak"] * 1e9 / eng.target.config.weight_bytes(), 1),
+        "weight_stream_roofline_tokens_per_s": round(rf["peak"] * 1e9 / wb, 1),
         "e2e": {"value": round((len(out) - 1) / e2e_s, 2), "unit": "tokens/s",
                 "h2d_bytes_per_step": PROMPT_LEN * 16, "d2h_bytes_per_step": len(out) * 16,
-                "note": "generate() on host token lists, prefill included"},
+                "note": "generate() on a host token list, prefill included"},
         "gpu_launches": launches,
         "roofline": rf,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
-    return line
 
 
 def run_reference(args) -> dict:

@@ -23,6 +23,7 @@
 #ifndef SPECPIPE_B200_H
 #define SPECPIPE_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -263,6 +264,16 @@ int sp_stage_ld_vis(const sp_stage* s);
  * (without inserting its cells); visible counts = plan lengths - 1. */
 int sp_stage_plan_only(sp_stage* s, const sp_token* host_toks, int n,
                        int check_coverage, void* stream);
+
+/* Cross-process control plane (distributed pipeline): page-lock a host
+ * region (e.g. POSIX shared memory) and map it into the device address space
+ * so kernels can read cancel words and results can be written into it;
+ * ``sp_signal`` stores ``value`` to a mapped flag after all prior work on
+ * ``stream`` (CANCEL / LOGITS transport.py:265-271, engine.py:619-623). */
+int sp_host_register(void* ptr, size_t bytes, void** dev_ptr);
+int sp_host_unregister(void* ptr);
+int sp_signal(int* dev_flag, int value, void* stream);
+int sp_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 
 /* Library info. */
 const char* sp_version(void);

@@ -103,6 +103,10 @@ PROTOTYPES = {
     "sp_stage_plan_sync": (I, [P, P, P, I, P]),
     "sp_stage_ld_vis": (I, [P]),
     "sp_stage_plan_only": (I, [P, P, I, I, P]),
+    "sp_host_register": (I, [P, C.c_size_t, P]),
+    "sp_host_unregister": (I, [P]),
+    "sp_signal": (I, [P, I, P]),
+    "sp_copy_async": (I, [P, P, C.c_size_t, P]),
     "sp_version": (C.c_char_p, []),
     "sp_device_arch": (I, []),
 }

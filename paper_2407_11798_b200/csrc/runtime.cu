@@ -715,3 +715,40 @@ extern "C" int sp_device_arch(void) {
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
   return major * 10 + minor;
 }
+
+// ---------------------------------------------------------------------------
+// Cross-process control plumbing (distributed pipeline, dist.py).
+// ---------------------------------------------------------------------------
+
+namespace sp {
+// Completion signal for a result block copied into host-mapped memory: the
+// copy precedes this kernel in stream order; the flag store is made visible
+// system-wide after it (the head polls the flag, then reads the block).
+__global__ void signal_kernel(volatile int* flag, int value) {
+  __threadfence_system();
+  *flag = value;
+  __threadfence_system();
+}
+}  // namespace sp
+
+extern "C" int sp_host_register(void* ptr, size_t bytes, void** dev_ptr) {
+  if (!ptr || !bytes || !dev_ptr) return SP_ERR_ARG;
+  SP_CHECK(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+  SP_CHECK(cudaHostGetDevicePointer(dev_ptr, ptr, 0));
+  return SP_OK;
+}
+
+extern "C" int sp_host_unregister(void* ptr) {
+  return cuda_status(cudaHostUnregister(ptr));
+}
+
+extern "C" int sp_signal(int* dev_flag, int value, void* stream) {
+  if (!dev_flag) return SP_ERR_ARG;
+  sp::signal_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(dev_flag, value);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int sp_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault,
+                                     reinterpret_cast<cudaStream_t>(stream)));
+}

@@ -1,0 +1,434 @@
+"""Multi-GPU pipeline: one process per B200 under torchrun.
+
+Rank r hosts pipeline stage r (a contiguous layer range from
+``plan_layer_split``); rank 0 also hosts the head and the draft (its own
+stream).  The reference's transactions (transport.py:234-271) map onto:
+
+* RUN_CONFIG / CACHE_COPY / CACHE_REMOVE / SHUTDOWN — records in a
+  single-writer ring in POSIX shared memory.  Every worker reads every record
+  in order and enqueues the matching work on its compute stream, so stream
+  order *is* the reference's per-stage transaction order.  The host never
+  waits for the GPU.
+* ACTIVATIONS — NCCL point-to-point ``isend``/``irecv`` between consecutive
+  ranks (NVLink), issued on the compute stream; the message carries the
+  M x d activations plus a status word (placeholder, engine.py:545-554).
+* CANCEL — words in the same shared region, page-locked and mapped into
+  every GPU's address space: the head's store overtakes all queued work
+  because kernels read the word when they execute (early cancellation).
+* LOGITS — the last rank copies its fused-head result block into the shared
+  region and raises a ready flag from the stream (``sp_signal``); the head
+  polls the flag (FIFO).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import struct
+import time
+import uuid
+from collections import deque
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+from .model import RowResult, TOKEN_DTYPE
+from .pipeline import RunResult
+from .runtime import RES_DTYPE, Stage
+
+# record types
+R_RUN, R_COPY, R_REMOVE, R_RESET, R_SHUTDOWN, R_MARK = 1, 2, 3, 4, 5, 6
+
+RING = 2048            # control records
+SLOT = 4096            # bytes per record (header + <= 254 tokens)
+CANCEL = 4096          # cancel words (run_id % CANCEL)
+RESULTS = 64           # result slots (>= runs in flight)
+ACT_RING = 16          # activation buffers per rank (>= runs in flight)
+PAGE = 4096
+
+
+def _align(n: int, a: int = PAGE) -> int:
+    return (n + a - 1) // a * a
+
+
+class ControlPlane:
+    """Shared-memory ring + cancel words + result blocks (one per job)."""
+
+    def __init__(self, name: str, create: bool, n_ranks: int, max_tokens: int,
+                 n_stat: int):
+        from multiprocessing import shared_memory
+        self.n_ranks = n_ranks
+        self.res_rows = 1 + n_stat + max_tokens
+        self.res_bytes = _align(self.res_rows * 16, 256)
+        self.off_ring = PAGE
+        self.off_cancel = self.off_ring + RING * SLOT
+        self.off_res = self.off_cancel + _align(CANCEL * 4)
+        self.off_flags = self.off_res + RESULTS * self.res_bytes
+        self.size = _align(self.off_flags + RESULTS * 4)
+        if create:
+            self.shm = shared_memory.SharedMemory(name=name, create=True, size=self.size)
+            self.shm.buf[:self.size] = b"\0" * self.size
+        else:
+            self.shm = shared_memory.SharedMemory(name=name, create=False)
+            try:  # only the creator owns (and unlinks) the segment
+                from multiprocessing import resource_tracker
+                resource_tracker.unregister(self.shm._name, "shared_memory")
+            except Exception:
+                pass
+        buf = self.shm.buf
+        self.hdr = np.ndarray((64,), dtype=np.int64, buffer=buf, offset=0)
+        self.ring = np.ndarray((RING, SLOT), dtype=np.uint8, buffer=buf, offset=self.off_ring)
+        self.cancel = np.ndarray((CANCEL,), dtype=np.int32, buffer=buf, offset=self.off_cancel)
+        self.res = np.ndarray((RESULTS, self.res_bytes // 4), dtype=np.int32, buffer=buf,
+                              offset=self.off_res)
+        self.flags = np.ndarray((RESULTS,), dtype=np.int32, buffer=buf, offset=self.off_flags)
+        self.base = self.hdr.ctypes.data   # offset 0 of the mapping
+        self.dev_base = None
+        self.creator = create
+        self.cursor = 0
+
+    # device mapping of [cancel .. flags] (page-aligned)
+    def register(self) -> None:
+        lib = _lib.load()
+        dev = C.c_void_p()
+        n = self.size - self.off_cancel
+        check(lib.sp_host_register(self.base + self.off_cancel, n, C.byref(dev)),
+              "sp_host_register")
+        self.dev_base = dev.value - self.off_cancel
+
+    def dev(self, off: int) -> int:
+        return self.dev_base + off
+
+    def cancel_dev(self) -> int:
+        return self.dev(self.off_cancel)
+
+    def res_dev(self, slot: int) -> int:
+        return self.dev(self.off_res + slot * self.res_bytes)
+
+    def flag_dev(self, slot: int) -> int:
+        return self.dev(self.off_flags + 4 * slot)
+
+    # -- writer (rank 0) ---------------------------------------------------------
+    def write(self, rtype: int, payload: bytes) -> None:
+        idx = int(self.hdr[1])
+        while True:
+            lag = min(int(self.hdr[8 + r]) for r in range(1, self.n_ranks))
+            if idx - lag < RING:
+                break
+            time.sleep(0)
+        if len(payload) + 8 > SLOT:
+            raise ValueError("control record too large")
+        rec = self.ring[idx % RING]
+        rec[:8] = np.frombuffer(struct.pack("<ii", rtype, len(payload)), dtype=np.uint8)
+        rec[8:8 + len(payload)] = np.frombuffer(payload, dtype=np.uint8)
+        self.hdr[1] = idx + 1          # publish (x86-TSO: record stores land first)
+
+    # -- readers (ranks >= 1) ------------------------------------------------------
+    def read(self, rank: int):
+        idx = self.cursor
+        while int(self.hdr[1]) <= idx:
+            time.sleep(0)
+        rec = self.ring[idx % RING]
+        rtype, n = struct.unpack("<ii", rec[:8].tobytes())
+        payload = rec[8:8 + n].tobytes()
+        self.cursor = idx + 1
+        self.hdr[8 + rank] = self.cursor
+        return rtype, payload
+
+    def close(self, unlink: bool = False) -> None:
+        try:
+            if self.dev_base is not None:
+                _lib.load().sp_host_unregister(C.c_void_p(self.base + self.off_cancel))
+                self.dev_base = None
+        except Exception:
+            pass
+        del self.hdr, self.ring, self.cancel, self.res, self.flags
+        try:
+            self.shm.close()
+        except BufferError:   # a caller still holds a view; the OS unmaps at exit
+            pass
+        if unlink:
+            self.shm.unlink()
+
+
+def _pack_run(run_id, kind, flags, toks: np.ndarray, rows) -> bytes:
+    r = np.asarray(rows, dtype=np.int32)
+    return (struct.pack("<iiiii", run_id, kind, flags, len(toks), len(r))
+            + r.tobytes() + np.ascontiguousarray(toks, dtype=TOKEN_DTYPE).tobytes())
+
+
+def _unpack_run(p: bytes):
+    run_id, kind, flags, n, nr = struct.unpack("<iiiii", p[:20])
+    rows = np.frombuffer(p[20:20 + 4 * nr], dtype=np.int32)
+    toks = np.frombuffer(p[20 + 4 * nr:20 + 4 * nr + 16 * n], dtype=TOKEN_DTYPE).copy()
+    return run_id, kind, flags, toks, rows
+
+
+class _StageRank:
+    """Per-rank stage state shared by the head side and the worker loop."""
+
+    def __init__(self, model, lo, hi, rank, world, plane: ControlPlane, cfg_part,
+                 capacity, max_tokens):
+        import torch
+        self.rank, self.world = rank, world
+        self.plane = plane
+        self.stream = torch.cuda.Stream(model.device)
+        self.stage = Stage(model, lo, hi, capacity=capacity, max_tokens=max_tokens,
+                           n_seq_ids=cfg_part, stream=self.stream,
+                           cancel_table=plane.cancel_dev(), cancel_size=CANCEL)
+        d = model.config.embed_dim
+        self.d = d
+        self.words = max_tokens * d + 4
+        self.inbuf = torch.zeros((ACT_RING, self.words), dtype=torch.float32, device=model.device)
+        self.outbuf = torch.zeros((ACT_RING, self.words), dtype=torch.float32, device=model.device)
+        self.res = torch.zeros((RESULTS, plane.res_rows, 4), dtype=torch.int32,
+                               device=model.device)
+        self.works = deque()
+        torch.cuda.synchronize(model.device)
+
+    def _reap(self) -> None:
+        while self.works and self.works[0].is_completed():
+            self.works.popleft()
+
+    def run(self, run_id, kind, flags, toks, rows) -> None:
+        import torch
+        import torch.distributed as dist
+        n = len(toks)
+        k = run_id % ACT_RING
+        nw = n * self.d + 4
+        xin = self.inbuf[k]
+        xout = self.outbuf[k]
+        with torch.cuda.stream(self.stream):
+            if self.rank > 0:
+                dist.irecv(xin[:nw], src=self.rank - 1).wait()
+            self.stage.forward(toks, run_id, kind, flags,
+                               x_in=xin.data_ptr() if self.rank > 0 else None,
+                               in_status=xin[n * self.d:].data_ptr() if self.rank > 0 else None,
+                               x_out=xout.data_ptr(),
+                               out_status=xout[n * self.d:].data_ptr())
+            if self.rank < self.world - 1:
+                self.works.append(dist.isend(xout[:nw], dst=self.rank + 1))
+            else:
+                self._emit_result(run_id, n, rows, xout)
+        self._reap()
+
+    def _emit_result(self, run_id, n, rows, xout) -> None:
+        lib = self.stage.lib
+        slot = run_id % RESULTS
+        blk = self.res[slot]
+        s = self.stream.cuda_stream
+        # header: [status, err, n_rows, run_id]; stage status row; rows
+        check(lib.sp_copy_async(blk[0].data_ptr(), xout[n * self.d:].data_ptr(), 4, s))
+        if len(rows):
+            self.stage.lmhead(list(rows), x=xout.data_ptr(),
+                              out=blk[2:].data_ptr(), err_out=blk[0, 1:].data_ptr())
+        nbytes = 16 * (2 + len(rows))
+        check(lib.sp_copy_async(self.plane.res_dev(slot), blk.data_ptr(), nbytes, s))
+        check(lib.sp_signal(self.plane.flag_dev(slot), run_id, s))
+
+    def copy(self, src, dst_mask, end) -> None:
+        dsts = [i for i in range(32) if (dst_mask >> i) & 1]
+        self.stage.cache_copy(src, dsts, end)
+
+    def remove(self, seq, frm) -> None:
+        self.stage.cache_remove(seq, frm)
+
+
+def worker_loop(model, lo, hi, rank, world, plane: ControlPlane, partitions,
+                capacity, max_tokens, on_mark=None) -> None:
+    """Ranks >= 1: serve control records until SHUTDOWN (never blocks on the GPU)."""
+    import torch
+    sr = _StageRank(model, lo, hi, rank, world, plane, partitions, capacity, max_tokens)
+    while True:
+        rtype, p = plane.read(rank)
+        if rtype == R_RUN:
+            sr.run(*_unpack_run(p))
+        elif rtype == R_COPY:
+            sr.copy(*struct.unpack("<iIi", p[:12]))
+        elif rtype == R_REMOVE:
+            sr.remove(*struct.unpack("<ii", p[:8]))
+        elif rtype == R_RESET:
+            sr.stage.reset()
+            sr.stream.synchronize()
+        elif rtype == R_MARK:
+            sr.stream.synchronize()
+            if on_mark is not None:
+                on_mark(struct.unpack("<i", p[:4])[0])
+        elif rtype == R_SHUTDOWN:
+            sr.stream.synchronize()
+            while sr.works:
+                sr.works.popleft().wait()
+            torch.cuda.synchronize()
+            return
+
+
+class DistPipeline:
+    """Head-side pipeline over torchrun ranks (rank 0 = head + stage 0)."""
+
+    def __init__(self, model, ranges, plane: ControlPlane, world: int, partitions=8,
+                 capacity=8192, max_tokens=256):
+        self.plane = plane
+        self.world = world
+        lo, hi = ranges[0]
+        self.sr = _StageRank(model, lo, hi, 0, world, plane, partitions, capacity,
+                             max_tokens)
+        self.stages = [self.sr.stage]
+        self.fifo: deque = deque()
+        self.n_stat = (world + 3) // 4
+
+    @property
+    def n_stages(self) -> int:
+        return self.world
+
+    def reset(self) -> None:
+        if self.fifo:
+            raise RuntimeError("reset with runs in flight")
+        self.plane.write(R_RESET, b"")
+        self.sr.stage.reset()
+        self.sr.stream.synchronize()
+        self.plane.cancel[:] = 0
+        self.plane.flags[:] = 0
+
+    def mark(self, tag: int) -> None:
+        self.plane.write(R_MARK, struct.pack("<i", tag))
+
+    def launch(self, run_id, kind, toks, flags, rows) -> None:
+        if len(self.fifo) >= RESULTS:
+            raise RuntimeError("too many runs in flight")
+        self.plane.write(R_RUN, _pack_run(run_id, kind, flags, toks, rows))
+        self.sr.run(run_id, kind, flags, toks, rows)
+        self.fifo.append((run_id, len(rows)))
+
+    def copy(self, src, dsts, end_pos) -> None:
+        m = 0
+        for d in dsts:
+            m |= 1 << int(d)
+        self.plane.write(R_COPY, struct.pack("<iIi", src, m, end_pos))
+        self.sr.copy(src, m, end_pos)
+
+    def remove(self, seq, from_pos) -> None:
+        self.plane.write(R_REMOVE, struct.pack("<ii", seq, from_pos))
+        self.sr.remove(seq, from_pos)
+
+    def cancel_run(self, run_id: int) -> None:
+        self.plane.cancel[run_id % CANCEL] = run_id
+
+    def ready(self) -> bool:
+        if not self.fifo:
+            return False
+        run_id = self.fifo[0][0]
+        return int(self.plane.flags[run_id % RESULTS]) == run_id
+
+    def _collect(self) -> RunResult:
+        run_id, nrow = self.fifo.popleft()
+        blk = self.plane.res[run_id % RESULTS]
+        status = int(blk[0])
+        err = int(blk[1])
+        rows = []
+        if status == _lib.SP_STATUS_VALID and nrow:
+            rr = blk[8:8 + 4 * nrow].view(RES_DTYPE).reshape(-1)
+            rows = [RowResult(r["a"], r["b"], r["c"], r["d"]) for r in rr]
+        return RunResult(run_id, status == _lib.SP_STATUS_PLACEHOLDER, rows, err,
+                         [status] * self.world)
+
+    def poll(self) -> Optional[RunResult]:
+        return self._collect() if self.ready() else None
+
+    def wait(self) -> RunResult:
+        if not self.fifo:
+            raise RuntimeError("wait with an empty FIFO")
+        while not self.ready():
+            time.sleep(0)
+        return self._collect()
+
+    def in_flight(self) -> int:
+        return len(self.fifo)
+
+    def shutdown(self) -> None:
+        self.plane.write(R_SHUTDOWN, b"")
+        self.sr.stream.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# process-level setup
+# ---------------------------------------------------------------------------
+
+def init(max_tokens: int = 256):
+    """torchrun bootstrap: NCCL for activations, gloo for host control."""
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gloo = dist.new_group(backend="gloo")
+    name = [f"sp_{os.getpid()}_{uuid.uuid4().hex[:8]}" if rank == 0 else None]
+    dist.broadcast_object_list(name, src=0, group=gloo)
+    n_stat = (world + 3) // 4
+    plane = ControlPlane(name[0], rank == 0, world, max_tokens, n_stat)
+    dist.barrier(group=gloo)
+    if rank != 0:
+        plane = ControlPlane(name[0], False, world, max_tokens, n_stat)
+    plane.register()
+    dist.barrier(group=gloo)
+    return rank, world, local, plane, gloo
+
+
+def build_slice(cfg, rank: int, world: int, node_weights=None):
+    """This rank's layer range and weights (plan_layer_split, engine.py:186-224)."""
+    import torch
+    from .engine import plan_layer_split
+    from .model import build_model
+    tc = cfg.target_config()
+    ranges = plan_layer_split(tc.n_layers, world, node_weights)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    model = build_model(tc, dev, layer_range=ranges[rank])
+    return model, ranges
+
+
+def bench_main(args):
+    """bench.py under torchrun (N > 1): rank 0 runs the head, the others serve."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local, plane, gloo = init()
+    import bench as B
+    from .engine import Engine, ExperimentConfig
+    from .model import build_model, sample_prompt
+    cfg = ExperimentConfig(mode="async-speculative", nodes=world + 1,
+                           target_shape=B.TARGET, draft_shape=B.DRAFT,
+                           draft_backend="synthetic", alpha=B.ALPHA,
+                           prompt_len=B.PROMPT_LEN, gen_len=args.gen_len,
+                           max_context=B.MAX_CTX, target_seed=1, draft_seed=2,
+                           capacity=8192, node_weights=getattr(args, "node_weights", None))
+    model, ranges = build_slice(cfg, rank, world, cfg.node_weights)
+    marks = []
+    if rank != 0:
+        lo, hi = ranges[rank]
+        worker_loop(model, lo, hi, rank, world, plane, cfg.partitions, cfg.capacity,
+                    cfg.max_run_tokens, on_mark=lambda t: marks.append((t, time.perf_counter())))
+        out = [None]
+        t = {m: v for m, v in marks}
+        dist.gather_object((t.get(1), t.get(2)), None, dst=0, group=gloo)
+        dist.barrier(group=gloo)
+        plane.close()
+        dist.destroy_process_group()
+        return None
+    dev = torch.device("cuda", local)
+    draft = build_model(cfg.draft_config(), dev)
+    pipe = DistPipeline(model, ranges, plane, world, cfg.partitions, cfg.capacity,
+                        cfg.max_run_tokens)
+    eng = Engine(cfg, target_model=model, draft_model=draft, pipeline=pipe)
+    line = B.measure(eng, args, n_gpus=world, pipe=pipe)
+    pipe.shutdown()
+    times = [None] * world
+    dist.gather_object((None, None), times, dst=0, group=gloo)
+    spans = [t1 - t0 for (t0, t1) in times[1:] if t0 is not None and t1 is not None]
+    line["rank_spans_s"] = [round(x, 4) for x in spans]
+    dist.barrier(group=gloo)
+    plane.close(unlink=True)
+    dist.destroy_process_group()
+    return line

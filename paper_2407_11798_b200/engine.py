@@ -346,6 +346,7 @@ class Head:
         self.bytes: Dict[str, int] = {}
         self.msgs: Dict[Tuple[int, str], int] = {}
         self.stage_logs: Dict[int, list] = {i + 1: [] for i in range(pipe.n_stages)}
+        self.tips: Optional[list] = None   # NS-run tips (truth tables)
         self._t0 = time.perf_counter()
 
     def now(self) -> float:
@@ -494,6 +495,8 @@ class Head:
         if self.draft is not None:
             self._draft_reply()
         t0 = greedy_sample(res.rows[0])
+        if self.tips is not None:
+            self.tips.append(res.rows[0])
         self.accepted.append(t0)
         self.generated += 1
         if self.cfg.eos_token is not None and t0 == self.cfg.eos_token:
@@ -520,6 +523,8 @@ class Head:
             res = self._recv()
             got = self._pop_record(res)
             got.status = COMPLETED
+            if self.tips is not None:
+                self.tips.append(res.rows[0])
             result = verify_run(got, res.rows, self.accepted, eos_token=self.cfg.eos_token)
             if result.next_token is None:
                 raise ProtocolError("iterative run produced no next token")
@@ -857,8 +862,7 @@ class Engine:
         if cfg.draft_backend == "synthetic":
             key = hash(tuple(prompt))
             if key not in self._tables:
-                self._tables[key] = truth_table(self.target, prompt,
-                                                cfg.gen_len + 16)
+                self._tables[key] = self.truth(prompt, cfg.gen_len + 16)
             truth, runner = self._tables[key]
             seed = cfg.draft_seed * 1000003 + prompt_seed
             prev = getattr(self, "_table_draft", None)
@@ -883,8 +887,6 @@ class Engine:
         seed = cfg.prompt_seed if prompt_seed is None else prompt_seed
         if prompt is None:
             prompt = sample_prompt(seed, cfg.prompt_len, self.target.config.vocab_size)
-        if mode is not None and cfg.n_stages() != self.pipe.n_stages:
-            raise EngineError("mode override must keep the pipeline depth")
         self.pipe.reset()
         draft = self._make_draft(prompt, seed)
         wall0 = time.perf_counter()
@@ -905,6 +907,23 @@ class Engine:
                          accept_events=list(head.accept_events),
                          cancel_log=list(head.cancel_log), node_logs=node_logs,
                          consumed=dict(sent), sent=sent, records=list(head.records))
+
+    def truth(self, prompt: List[int], n: int):
+        """Greedy stream and runner-ups of the target along the true path,
+        computed by an iterative pass through this engine's own pipeline:
+        ``truth[p]``/``runner[p]`` are the greedy token / runner-up predicted
+        for absolute position p (synthetic-draft table)."""
+        n = min(n, self.cfg.max_context - len(prompt) - 1)
+        cfg = replace(self.cfg, mode="iterative", gen_len=n, eos_token=None,
+                      prompt_len=len(prompt))
+        self.pipe.reset()
+        head = Head(cfg, self.pipe, None, prompt, self.target.config.embed_dim)
+        head.tips = []
+        head.run_iterative()
+        self.pipe.reset()
+        truth = list(prompt) + [r.argmax for r in head.tips]
+        runner = [0] * len(prompt) + [r.second for r in head.tips]
+        return truth, runner
 
     def launch_count(self) -> int:
         """Kernels this process has launched through the C ABI so far."""
