@@ -151,69 +151,66 @@ def cpu_baseline(n_decode: int = 3, layers: int = 2, prompt_len: int = 16) -> di
 # roofline: the dominant kernel (weight-streaming GEMV) timed with CUDA events
 # ---------------------------------------------------------------------------
 
-def gemv_roofline(engine, reps: int = 3) -> dict:
-    """Time the full M=1 GEMV set of one decode token (4 GEMVs x L layers of
-    this rank's stage + LM head if present) with CUDA events on the stage
-    stream.  Algorithmic bytes = weight bytes + activation bytes."""
+def gemv_roofline(engine, reps: int = 5) -> dict:
+    """Roofline of the dominant kernel: the weight-streaming GEMM of every
+    decoder layer of this rank's stage (QKV, O, gate/up, down; tcgen05 path
+    for bf16 weights), one decode token (M=1), each launch timed with CUDA
+    events on the stage stream after capture into a CUDA graph (so host
+    launch gaps are excluded).  Algorithmic bytes per launch = the weight
+    matrix + its activation row in and out; weights (>= 8 GB per stage) are
+    far larger than the 126 MB L2."""
+    import ctypes as C
     import torch
     from paper_2407_11798_b200 import _lib
-    from paper_2407_11798_b200.model import TOKEN_DTYPE
-    import ctypes as C
-    import numpy as np
     st = engine.pipe.stages[0]
-    cfg = st.cfg
-    lib = st.lib
+    cfg, lib = st.cfg, st.lib
     d, f = cfg.embed_dim, cfg.hidden
     q, kv = cfg.n_heads * cfg.head_dim, cfg.kv_dim
     dev = st.device
-    x = torch.randn((8, max(d, f)), device=dev, dtype=torch.float32)
-    out = torch.zeros((8, 2 * f + q + 2 * kv), device=dev, dtype=torch.float32)
-    toks = torch.zeros(8 * 4, dtype=torch.int32, device=dev)
-    kc = torch.zeros((16, kv), dtype=torch.bfloat16, device=dev)
-    wb = 2
-    launches = []
+    X = torch.zeros((256, max(d, f)), device=dev, dtype=torch.bfloat16).normal_()
+    out = torch.zeros((256, 2 * f + q + 2 * kv), device=dev, dtype=torch.float32)
+    scratch = torch.zeros(8 << 20, device=dev)
+    tick = torch.zeros(4096, dtype=torch.int32, device=dev)
+    args, nbytes = [], 0
     for l in range(st.lo, st.hi):
         L = engine.target.layers[l]
-        launches.append((L["qkv"], q + 2 * kv, d, _lib.SP_EPI_QKV, 1))
-        launches.append((L["o"], d, q, _lib.SP_EPI_RESID, 0))
-        launches.append((L["up"], 2 * f, d, _lib.SP_EPI_SWIGLU, 1))
-        launches.append((L["down"], d, f, _lib.SP_EPI_RESID, 0))
-    args = []
-    nbytes = 0
-    for w, n, k, epi, norm in launches:
-        a = _lib.sp_gemv_args()
-        a.w, a.w_dtype, a.n_rows, a.k = w.data_ptr(), _lib.SP_DTYPE_BF16, n, k
-        a.x, a.m, a.ldx = x.data_ptr(), 1, x.shape[1]
-        a.norm, a.norm_eps, a.gain = norm, 1e-5, None
-        a.epi, a.out, a.ldo = epi, out.data_ptr(), out.shape[1]
-        a.q_rows, a.kv_rows, a.k_cache, a.v_cache = q, kv, kc.data_ptr(), kc.data_ptr()
-        a.cache_row0, a.rope, a.head_dim, a.rope_theta = 0, 1, cfg.head_dim, 10000.0
-        a.toks, a.err, a.run_state = toks.data_ptr(), None, None
-        args.append(a)
-        nbytes += n * k * wb + 4 * (k + n)
-    s = st.stream
+        for key, n, k in (("qkv", q + 2 * kv, d), ("o", d, q), ("up", 2 * f, d),
+                          ("down", d, f)):
+            a = _lib.sp_tc_args()
+            a.w, a.n_rows, a.k, a.m, a.epi = L[key].data_ptr(), n, k, 1, _lib.SP_EPI_STORE
+            a.out, a.ldo = out.data_ptr(), out.shape[1]
+            a.scratch, a.tickets = scratch.data_ptr(), tick.data_ptr()
+            args.append(a)
+            nbytes += n * k * 2 + 2 * k + 4 * n
+    s = torch.cuda.Stream(dev)
+    graph = torch.cuda.CUDAGraph()
+    for a in args:   # warm (first launches configure smem attributes)
+        _lib.check(lib.sp_tc_gemm(C.byref(a), X.data_ptr(), 256, s.cuda_stream))
+    s.synchronize()
+    with torch.cuda.graph(graph, stream=s):
+        for a in args:
+            _lib.check(lib.sp_tc_gemm(C.byref(a), X.data_ptr(), 256, s.cuda_stream))
     times = []
     for rep in range(reps + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        for a in args:
-            _lib.check(lib.sp_gemv(C.byref(a), s.cuda_stream))
+        graph.replay()
         e1.record(s)
         e1.synchronize()
         if rep:
             times.append(e0.elapsed_time(e1) / 1e3)
-    t = min(times)
+    t = statistics.median(times)
     peak, how = _peaks()
     achieved = nbytes / t / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_gemv_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
             traffic = json.load(fh).get("bytes_per_launch")
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
             "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-            "kernel": "gemv_kernel<bf16,MT=1> (QKV+O+gate/up+down of every layer of the "
-                      "stage, one decode token)",
+            "kernel": "tc_gemm_kernel<NT=16> (tcgen05+TMEM, bulk-copied tiled bf16 "
+                      "weights; QKV+O+gate/up+down of every layer of the stage, M=1)",
             "algorithmic_bytes_per_launch": round(nbytes / len(args)),
             "avg_launch_us": round(t / len(args) * 1e6, 2), "launches": len(args),
             "peak_source": how}

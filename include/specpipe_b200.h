@@ -152,6 +152,49 @@ typedef struct sp_gemv_args {
 
 int sp_gemv(const sp_gemv_args* a, void* stream);
 
+/* Skinny tensor-core GEMM (tcgen05 + TMEM + TMA, bf16 weights/activations,
+ * fp32 accumulate) used for every bf16 run: D[rows, tokens] = W . X^T with
+ * split-K merged in fixed order and the epilogues of the GEMV family.
+ * RMSNorm enters as a per-token scale from sum-of-squares partials
+ * (ss_in[p * ss_ld + token], p < ss_nparts); the residual epilogue emits the
+ * next norm's bf16 input (xb_next = x * gain_next) and its partials. */
+typedef struct sp_tc_args {
+  const void* w;           /* bf16 weights in the TILED layout: [n_rows/128]
+                              [k/64] tiles of 128 x 64, each stored as the
+                              128B-swizzled K-major smem image (16 KB)      */
+  int32_t n_rows;          /* multiple of 128                               */
+  int32_t k;               /* multiple of 64                                */
+  int32_t m;               /* tokens                                        */
+  int32_t tok0;            /* first token of the launch (internal)          */
+  int32_t epi;             /* SP_EPI_STORE | QKV | SWIGLU | RESID            */
+  int32_t norm;
+  float norm_eps;
+  void* out;               /* STORE/QKV-q: f32; SWIGLU: bf16; RESID: f32 x  */
+  int32_t ldo;
+  int32_t q_rows, kv_rows; /* QKV                                           */
+  void* k_cache;           /* bf16 [cap, kv_rows]                           */
+  void* v_cache;
+  int32_t cache_row0;
+  int32_t head_dim;
+  float rope_theta;
+  const sp_token* toks;
+  const float* ss_in;      /* norm statistic partials                       */
+  int32_t ss_nparts;
+  int32_t ss_ld;
+  float* ss_out;           /* RESID: per-128-row-tile partials              */
+  void* xb_next;           /* RESID: bf16 [tokens, ldo]                     */
+  const float* gain_next;  /* RESID: gain of the next RMSNorm (or NULL)     */
+  float* scratch;          /* split-K partials                              */
+  int* tickets;            /* per row tile, zero-initialised                */
+  int32_t ksplit;          /* 0 = auto                                      */
+  int* err;
+  const int* run_state;
+} sp_tc_args;
+
+/* Low-level form (tests): a->w tiled bf16; X bf16 [x_rows, k] row-major
+ * with x_rows >= 128 allocated rows. */
+int sp_tc_gemm(const sp_tc_args* a, const void* x, int x_rows, void* stream);
+
 /* K4: per query, the position-ordered visible cell rows (ties by row),
  * the query's own row appended last.  model.py:287-323.  Rows >= row0
  * are the batch's own cells (described by ``toks``).                     */

@@ -62,6 +62,19 @@ class sp_gemv_args(C.Structure):
                 ("run_id", C.c_int32)]
 
 
+class sp_tc_args(C.Structure):
+    _fields_ = [("w", C.c_void_p), ("n_rows", C.c_int32), ("k", C.c_int32), ("m", C.c_int32),
+                ("tok0", C.c_int32), ("epi", C.c_int32), ("norm", C.c_int32),
+                ("norm_eps", C.c_float), ("out", C.c_void_p), ("ldo", C.c_int32),
+                ("q_rows", C.c_int32), ("kv_rows", C.c_int32), ("k_cache", C.c_void_p),
+                ("v_cache", C.c_void_p), ("cache_row0", C.c_int32), ("head_dim", C.c_int32),
+                ("rope_theta", C.c_float), ("toks", C.c_void_p), ("ss_in", C.c_void_p),
+                ("ss_nparts", C.c_int32), ("ss_ld", C.c_int32), ("ss_out", C.c_void_p),
+                ("xb_next", C.c_void_p), ("gain_next", C.c_void_p), ("scratch", C.c_void_p),
+                ("tickets", C.c_void_p), ("ksplit", C.c_int32), ("err", C.c_void_p),
+                ("run_state", C.c_void_p)]
+
+
 P = C.c_void_p
 I = C.c_int
 U32 = C.c_uint32
@@ -71,6 +84,7 @@ F = C.c_float
 PROTOTYPES = {
     "sp_embed": (I, [P, P, P, P, I, P, P, P]),
     "sp_gemv": (I, [P, P]),
+    "sp_tc_gemm": (I, [P, P, I, P]),
     "sp_build_plan": (I, [P, P, I, I, P, I, I, P, P, I, I, P, P]),
     "sp_attention": (I, [P, P, P, I, P, P, I, I, I, I, I, I, P, P, P, P, P]),
     "sp_kv_meta_write": (I, [P, P, I, P, I, I, I, P, P]),

@@ -23,6 +23,8 @@ plan_kernel(const int32_t* __restrict__ cell_pos,
             const sp_token* __restrict__ toks, int n, int max_context,
             int32_t* __restrict__ vis, int32_t* __restrict__ vis_len,
             int ld_vis, int check_cov, int* err, const int* run_state) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ int cnt[];  // [max_context + 1]
   // a run skipped by its gate is never checked (engine.py:581-590: the
   // coverage check follows the cancellation test)
@@ -115,6 +117,8 @@ constexpr int ATT_UNROLL = 4;
 
 template <typename T, int HD>
 __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int VEC = 16 / sizeof(T);
   constexpr int LPR = HD / VEC;           // lanes per row
   constexpr int G = ATT_THREADS / LPR;    // rows in flight per pass
@@ -226,12 +230,16 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
   for (int j = 0; j < VEC; ++j) part[g][l * VEC + j] = acc[j];
   __syncthreads();
 
-  float* outp = a.out + (size_t)i * a.H * HD + h * HD;
+  const size_t obase = (size_t)i * a.H * HD + h * HD;
+  auto store = [&](int d, float v) {
+    if (a.out_bf16) reinterpret_cast<__nv_bfloat16*>(a.out)[obase + d] = __float2bfloat16_rn(v);
+    else a.out[obase + d] = v;
+  };
   if (ns == 1) {
     for (int d = tid; d < HD; d += ATT_THREADS) {
       float o = part[0][d];
       for (int gg = 1; gg < G; ++gg) o += part[gg][d];
-      outp[d] = o / sum;
+      store(d, o / sum);
     }
     return;
   }
@@ -265,7 +273,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
       const float* b = base + ss * (HD + 2);
       o += ld_volatile_f(b + 2 + d) * __expf(ld_volatile_f(b) - M);
     }
-    outp[d] = o / L;
+    store(d, o / L);
   }
   if (tid == 0) a.tickets[i * a.H + h] = 0;
 }
@@ -274,14 +282,13 @@ template <typename T>
 static cudaError_t attn_dispatch(const AttnArgs& a, int hd, cudaStream_t st) {
   const dim3 grid(a.H, a.n, a.nsplit);
   switch (hd) {
-    case 8: attn_kernel<T, 8><<<grid, ATT_THREADS, 0, st>>>(a); break;
-    case 16: attn_kernel<T, 16><<<grid, ATT_THREADS, 0, st>>>(a); break;
-    case 32: attn_kernel<T, 32><<<grid, ATT_THREADS, 0, st>>>(a); break;
-    case 64: attn_kernel<T, 64><<<grid, ATT_THREADS, 0, st>>>(a); break;
-    case 128: attn_kernel<T, 128><<<grid, ATT_THREADS, 0, st>>>(a); break;
+    case 8: return launch_pdl(attn_kernel<T, 8>, grid, dim3(ATT_THREADS), 0, st, a);
+    case 16: return launch_pdl(attn_kernel<T, 16>, grid, dim3(ATT_THREADS), 0, st, a);
+    case 32: return launch_pdl(attn_kernel<T, 32>, grid, dim3(ATT_THREADS), 0, st, a);
+    case 64: return launch_pdl(attn_kernel<T, 64>, grid, dim3(ATT_THREADS), 0, st, a);
+    case 128: return launch_pdl(attn_kernel<T, 128>, grid, dim3(ATT_THREADS), 0, st, a);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
@@ -296,10 +303,9 @@ cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
                          (int)smem);
     configured = (int)smem;
   }
-  plan_kernel<<<n, PLAN_THREADS, smem, st>>>(cell_pos, cell_mask, n_old, row0,
-                                             toks, n, max_context, vis, vis_len,
-                                             ld_vis, check_cov, err, run_state);
-  return cudaGetLastError();
+  return launch_pdl(plan_kernel, dim3(n), dim3(PLAN_THREADS), smem, st, cell_pos, cell_mask,
+                    n_old, row0, toks, n, max_context, vis, vis_len, ld_vis, check_cov, err,
+                    run_state);
 }
 
 cudaError_t launch_attention(const AttnArgs& a, int kv_dtype, int hd,

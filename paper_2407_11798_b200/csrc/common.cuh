@@ -93,10 +93,39 @@ __device__ __forceinline__ bool run_skipped(const int* run_state) {
   return run_state != nullptr && ld_volatile(run_state) != 0;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with
+// launch_pdl() may start while its predecessor drains; it must call
+// pdl_wait() before reading anything the predecessor writes, and calls
+// pdl_trigger() to let its own successor start early.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ float gelu_tanh(float v) {
   // model.py:192-194 (tanh approximation)
   return 0.5f * v * (1.0f + tanhf(0.7978845608028654f * (v + 0.044715f * v * v * v)));
 }
 __device__ __forceinline__ float silu(float v) { return v / (1.0f + __expf(-v)); }
+
+bool pdl_enabled();
+
+template <typename Kernel, typename... Args>
+cudaError_t launch_pdl(Kernel kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 
 }  // namespace sp

@@ -14,6 +14,8 @@ __device__ __forceinline__ void store_cache(void* base, size_t idx, float v) {
 template <typename T, int MT, int ROWS, int EPI, bool NORM>
 __global__ void __launch_bounds__(GEMV_THREADS)
 gemv_kernel(const sp_gemv_args a) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ GemvSmem<T, MT, ROWS, NORM> sm;
   if (a.cancel_word != nullptr && blockIdx.x == 0 && threadIdx.x == 0 &&
       ld_volatile(a.cancel_word) == a.run_id)
@@ -90,10 +92,8 @@ template <typename T, int MT, int ROWS, int EPI>
 static cudaError_t launch_norm(const sp_gemv_args& a, cudaStream_t st) {
   const dim3 grid((a.n_rows + ROWS - 1) / ROWS);
   if (a.norm)
-    gemv_kernel<T, MT, ROWS, EPI, true><<<grid, GEMV_THREADS, 0, st>>>(a);
-  else
-    gemv_kernel<T, MT, ROWS, EPI, false><<<grid, GEMV_THREADS, 0, st>>>(a);
-  return cudaGetLastError();
+    return launch_pdl(gemv_kernel<T, MT, ROWS, EPI, true>, grid, dim3(GEMV_THREADS), 0, st, a);
+  return launch_pdl(gemv_kernel<T, MT, ROWS, EPI, false>, grid, dim3(GEMV_THREADS), 0, st, a);
 }
 
 template <typename T, int EPI>

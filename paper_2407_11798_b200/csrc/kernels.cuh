@@ -1,9 +1,13 @@
 // Launch interfaces shared by the kernel translation units and the runtime.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace sp {
+
+typedef sp_tc_args TcArgs;
 
 struct AttnArgs {
   const float* q;
@@ -22,6 +26,7 @@ struct AttnArgs {
   const int* cancel_word;  // device-visible cancel word of this run (or null)
   int run_id;
   int* err;
+  int out_bf16;            // write the output as bf16 (tensor-core path input)
 };
 
 struct LmPartial {
@@ -68,5 +73,10 @@ cudaError_t launch_copy(const int32_t* pos, uint32_t* mask, int n, int src,
 cudaError_t launch_remove(const int32_t* pos, uint32_t* mask, int n,
                           uint32_t seq_mask, int from_pos, cudaStream_t st);
 cudaError_t launch_keep(uint32_t* mask, int n, int seq, cudaStream_t st);
+bool make_map_bf16(CUtensorMap* map, const void* base, long rows, long cols, long ld_elems,
+                   int box_rows);
+cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st);
+int tc_nt_for(int m);
+int tc_ksplit(int n_rows, int k, int target_ctas);
 
 }  // namespace sp

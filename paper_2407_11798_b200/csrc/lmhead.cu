@@ -29,6 +29,8 @@ __device__ __forceinline__ void push(Top2& t, float v, int i) {
 
 template <typename T, int MT, int ROWS>
 __global__ void __launch_bounds__(GEMV_THREADS) lmhead_kernel(const LmArgs a) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ GemvSmem<T, MT, ROWS, true> sm;
   __shared__ int last;
   if (run_skipped(a.run_state)) {
@@ -139,14 +141,13 @@ __global__ void __launch_bounds__(GEMV_THREADS) lmhead_kernel(const LmArgs a) {
 cudaError_t launch_lmhead(const LmArgs& a, int w_dtype, cudaStream_t st) {
   constexpr int ROWS = 8;
   const dim3 grid((a.V + ROWS - 1) / ROWS);
+  const dim3 blk(GEMV_THREADS);
   if (w_dtype == SP_DTYPE_BF16) {
-    if (a.n_rows <= 1) lmhead_kernel<__nv_bfloat16, 1, ROWS><<<grid, GEMV_THREADS, 0, st>>>(a);
-    else lmhead_kernel<__nv_bfloat16, 4, ROWS><<<grid, GEMV_THREADS, 0, st>>>(a);
-  } else {
-    if (a.n_rows <= 1) lmhead_kernel<float, 1, ROWS><<<grid, GEMV_THREADS, 0, st>>>(a);
-    else lmhead_kernel<float, 4, ROWS><<<grid, GEMV_THREADS, 0, st>>>(a);
+    if (a.n_rows <= 1) return launch_pdl(lmhead_kernel<__nv_bfloat16, 1, ROWS>, grid, blk, 0, st, a);
+    return launch_pdl(lmhead_kernel<__nv_bfloat16, 4, ROWS>, grid, blk, 0, st, a);
   }
-  return cudaGetLastError();
+  if (a.n_rows <= 1) return launch_pdl(lmhead_kernel<float, 1, ROWS>, grid, blk, 0, st, a);
+  return launch_pdl(lmhead_kernel<float, 4, ROWS>, grid, blk, 0, st, a);
 }
 
 int lmhead_grid(int V) { return (V + 7) / 8; }

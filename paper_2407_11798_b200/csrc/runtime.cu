@@ -30,6 +30,8 @@ __global__ void embed_kernel(const T* __restrict__ emb,
                              const sp_token* __restrict__ toks, int n, int d,
                              int vocab, int max_context, float* __restrict__ x,
                              int* err, const int* run_state) {
+  pdl_wait();
+  pdl_trigger();
   if (run_skipped(run_state)) return;
   const int i = blockIdx.x;
   const sp_token t = toks[i];
@@ -54,6 +56,8 @@ __global__ void gate_kernel(sp_token* toks, int n, int kind, int flags,
                             const int* chain_tip, int* run_state,
                             int32_t* cell_pos, uint32_t* cell_mask, int row0,
                             int n_seq, int max_context, int* err) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int skip;
   if (threadIdx.x == 0) {
     int s = 0;
@@ -82,6 +86,8 @@ __global__ void gate_kernel(sp_token* toks, int n, int kind, int flags,
 __global__ void epilogue_kernel(const sp_token* toks, int n, const int* run_state,
                                 const int32_t* cell_pos, uint32_t* cell_mask,
                                 int n_cells, int row0, int* out_status) {
+  pdl_wait();
+  pdl_trigger();
   const int skip = ld_volatile(run_state);
   if (!skip) {
     if (out_status && blockIdx.x == 0 && threadIdx.x == 0) *out_status = SP_STATUS_VALID;
@@ -101,10 +107,49 @@ __global__ void epilogue_kernel(const sp_token* toks, int n, const int* run_stat
 __global__ void gather_rows_kernel(const float* __restrict__ x, int d,
                                    const int32_t* __restrict__ rows,
                                    float* __restrict__ out, const int* run_state) {
+  pdl_wait();
+  pdl_trigger();
   if (run_skipped(run_state)) return;
   const int r = blockIdx.x;
   const float* src = x + (size_t)rows[r] * d;
   for (int c = threadIdx.x; c < d; c += blockDim.x) out[(size_t)r * d + c] = src[c];
+}
+
+// Stage input for the tensor-core path: per token, the RMSNorm statistic of
+// x (fixed-order block reduction) and the bf16 normed-input row x * gain.
+__global__ void prep_kernel(const float* __restrict__ x, int d,
+                            const float* __restrict__ gain, __nv_bfloat16* __restrict__ xb,
+                            float* __restrict__ ss, const int* run_state) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[8];
+  if (run_skipped(run_state)) return;
+  const int t = blockIdx.x;
+  const float* xr = x + (size_t)t * d;
+  float s = 0.f;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    const float v = xr[c];
+    s = __fmaf_rn(v, v, s);
+    xb[(size_t)t * d + c] = __float2bfloat16_rn(gain ? __fmul_rn(v, gain[c]) : v);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) tot = __fadd_rn(tot, red[w]);
+    ss[t] = tot;
+  }
+}
+
+// Early inference cancellation (K14): one thread per observation point
+// folds the device-visible cancel word into run_state; kernels launched
+// after it skip.  A dedicated launch keeps every multi-CTA kernel's view of
+// run_state consistent (no mid-kernel flips).
+__global__ void observe_kernel(const int* cancel_word, int run_id, int* run_state) {
+  pdl_wait();
+  pdl_trigger();
+  if (ld_volatile(cancel_word) == run_id) *run_state = 1;
 }
 
 __global__ void chain_begin_kernel(const int* tip, int* gate, float cutoff,
@@ -126,6 +171,11 @@ __global__ void chain_begin_kernel(const int* tip, int* gate, float cutoff,
 
 using namespace sp;
 
+bool sp::pdl_enabled() {
+  static const bool on = getenv("SP_NO_PDL") == nullptr;
+  return on;
+}
+
 struct LayerW {
   const void* qkv = nullptr;
   const void* o = nullptr;
@@ -134,6 +184,10 @@ struct LayerW {
   const float* attn_norm = nullptr;
   const float* mlp_norm = nullptr;
 };
+
+static constexpr int TC_SCRATCH_FLOATS = 8 << 20;
+static constexpr int TC_TICKETS = 4096;
+static constexpr int OBSERVE_EVERY = 4;  // layers between cancel observations
 
 static constexpr int DESC_RING = 64;
 
@@ -148,6 +202,15 @@ struct sp_stage {
   const float* final_norm = nullptr;
   const int* cancel_table = nullptr;
   int cancel_size = 0;
+
+  bool tc = false;                       // bf16 llama path on tcgen05
+  __nv_bfloat16* xb = nullptr;           // [mt, d]   normed input (x * gain)
+  __nv_bfloat16* attnb = nullptr;        // [mt, q]   attention output
+  __nv_bfloat16* hb = nullptr;           // [mt, ffn] SwiGLU output
+  float* ss = nullptr;                   // [d/128, mt] sum-of-squares partials
+  float* tc_scratch = nullptr;
+  int* tc_tickets = nullptr;
+  CUtensorMap m_xb[2], m_attnb[2], m_hb[2];
 
   int32_t* cell_pos = nullptr;
   uint32_t* cell_mask = nullptr;
@@ -248,6 +311,30 @@ extern "C" int sp_stage_create(const sp_model_dims* dims, int layer_lo,
   alloc((void**)&s->run_state, sizeof(int));
   alloc((void**)&s->tip, sizeof(int) * 4);
   alloc((void**)&s->gate, sizeof(int));
+  // bf16 (llama) stages run on the tensor-core path with tiled weights
+  s->tc = d.arch == SP_ARCH_LLAMA && d.w_dtype == SP_DTYPE_BF16;
+  if (s->tc && (d.d_model % 128 || s->q_dim % 128 || (s->q_dim + 2 * s->kv_dim) % 128 ||
+                d.ffn_dim % 64)) {
+    delete s;
+    return SP_ERR_ARG;
+  }
+  if (s->tc) {
+    const int mtp = mt < 128 ? 128 : mt;   // TMA boxes of 128 rows
+    alloc((void**)&s->xb, 2 * (size_t)mtp * d.d_model);
+    alloc((void**)&s->attnb, 2 * (size_t)mtp * s->q_dim);
+    alloc((void**)&s->hb, 2 * (size_t)mtp * d.ffn_dim);
+    alloc((void**)&s->ss, sizeof(float) * (size_t)mt * (d.d_model / 128 + 1));
+    alloc((void**)&s->tc_scratch, sizeof(float) * (size_t)TC_SCRATCH_FLOATS);
+    alloc((void**)&s->tc_tickets, sizeof(int) * TC_TICKETS);
+    if (ok) {
+      const int boxes[2] = {16, 128};
+      for (int i = 0; i < 2 && ok; ++i) {
+        ok = make_map_bf16(&s->m_xb[i], s->xb, mtp, d.d_model, d.d_model, boxes[i]) &&
+             make_map_bf16(&s->m_attnb[i], s->attnb, mtp, s->q_dim, s->q_dim, boxes[i]) &&
+             make_map_bf16(&s->m_hb[i], s->hb, mtp, d.ffn_dim, d.ffn_dim, boxes[i]);
+      }
+    }
+  }
   alloc((void**)&s->desc_dev, sizeof(sp_token) * (size_t)mt * DESC_RING);
   alloc((void**)&s->rows_dev, sizeof(int32_t) * (size_t)mt * DESC_RING);
   if (ok && cudaMallocHost((void**)&s->desc_host, sizeof(sp_token) * (size_t)mt * DESC_RING) != cudaSuccess) ok = false;
@@ -269,7 +356,8 @@ extern "C" int sp_stage_destroy(sp_stage* s) {
   void* ptrs[] = {s->cell_pos, s->cell_mask, s->kc, s->vc, s->q, s->attn, s->h,
                   s->xg, s->vis, s->vis_len, s->att_scratch, s->att_tickets,
                   s->lm_scratch, s->lm_ticket, s->err, s->run_state, s->tip,
-                  s->gate, s->desc_dev, s->rows_dev};
+                  s->gate, s->desc_dev, s->rows_dev, s->xb, s->attnb, s->hb, s->ss,
+                  s->tc_scratch, s->tc_tickets};
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->desc_host) cudaFreeHost(s->desc_host);
   if (s->rows_host) cudaFreeHost(s->rows_host);
@@ -370,25 +458,22 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
                                ? s->cancel_table + (run_id % s->cancel_size)
                                : nullptr;
   if (!cont) {
-    gate_kernel<<<1, 128, 0, st>>>(dd, n, kind, flags, cancel_word, run_id,
-                                   in_status, chain ? s->gate : nullptr,
-                                   chain ? s->tip : nullptr,
-                                   s->run_state, s->cell_pos, s->cell_mask, row0,
-                                   s->n_seq, D.max_context, s->err);
-    SP_CHECK(cudaGetLastError());
+    SP_CHECK(launch_pdl(gate_kernel, dim3(1), dim3(128), 0, st, dd, n, kind, flags,
+                        cancel_word, run_id, in_status, chain ? (const int*)s->gate : nullptr,
+                        chain ? (const int*)s->tip : nullptr, s->run_state, s->cell_pos,
+                        s->cell_mask, row0, s->n_seq, D.max_context, s->err));
   }
 
   if (layer_a == 0) {
     const int threads = d >= 256 ? 256 : 64;
     if (D.w_dtype == SP_DTYPE_BF16)
-      embed_kernel<__nv_bfloat16><<<n, threads, 0, st>>>(
-          (const __nv_bfloat16*)s->emb, s->pos_table, dd, n, d, D.vocab,
-          D.max_context, x_out, s->err, s->run_state);
+      SP_CHECK(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(n), dim3(threads), 0, st,
+                          (const __nv_bfloat16*)s->emb, s->pos_table, (const sp_token*)dd, n, d,
+                          D.vocab, D.max_context, x_out, s->err, (const int*)s->run_state));
     else
-      embed_kernel<float><<<n, threads, 0, st>>>(
-          (const float*)s->emb, s->pos_table, dd, n, d, D.vocab, D.max_context,
-          x_out, s->err, s->run_state);
-    SP_CHECK(cudaGetLastError());
+      SP_CHECK(launch_pdl(embed_kernel<float>, dim3(n), dim3(threads), 0, st,
+                          (const float*)s->emb, s->pos_table, (const sp_token*)dd, n, d,
+                          D.vocab, D.max_context, x_out, s->err, (const int*)s->run_state));
   } else if (x_in != x_out) {
     SP_CHECK(cudaMemcpyAsync(x_out, x_in, sizeof(float) * (size_t)n * d,
                              cudaMemcpyDeviceToDevice, st));
@@ -414,59 +499,108 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
 
   const bool llama = D.arch == SP_ARCH_LLAMA;
   const size_t wb = wbytes(D);
+  if (s->tc) {
+    // bf16 normed input of layer_a's attention norm + its statistic
+    SP_CHECK(launch_pdl(prep_kernel, dim3(n), dim3(256), 0, st, (const float*)x_out, d,
+                        s->layers[layer_a - s->lo].attn_norm, s->xb, s->ss,
+                        (const int*)s->run_state));
+  }
+  int ss_parts = 1;
   for (int l = layer_a; l < layer_b; ++l) {
     const LayerW& L = s->layers[l - s->lo];
     void* kl = (char*)s->kc + wb * s->kv_layer_elems * (l - s->lo);
     void* vl = (char*)s->vc + wb * s->kv_layer_elems * (l - s->lo);
-    sp_gemv_args g{};
-    g.w_dtype = D.w_dtype;
-    g.run_state = s->run_state;
-    g.err = s->err;
-    g.toks = dd;
-    g.m = n;
-    // q, k, v (model.py:387-393): rmsnorm fused, k/v into cell rows
-    g.w = L.qkv; g.n_rows = s->q_dim + 2 * s->kv_dim; g.k = d;
-    g.x = x_out; g.ldx = d; g.norm = 1; g.norm_eps = D.norm_eps;
-    g.gain = llama ? L.attn_norm : nullptr;
-    g.epi = SP_EPI_QKV; g.out = s->q; g.ldo = s->q_dim;
-    g.q_rows = s->q_dim; g.kv_rows = s->kv_dim; g.k_cache = kl; g.v_cache = vl;
-    g.cache_row0 = row0; g.rope = llama ? 1 : 0; g.head_dim = D.head_dim;
-    g.rope_theta = D.rope_theta;
-    int rc = sp_gemv(&g, stream);
-    if (rc) return rc;
-    // attention over the plan (model.py:394-415)
     AttnArgs a{};
     a.q = s->q; a.k = kl; a.v = vl; a.vis = s->vis; a.vis_len = s->vis_len;
     a.ld_vis = s->ld_vis; a.n = n; a.H = D.n_heads; a.KH = D.n_kv_heads;
     a.nsplit = nsplit; a.scale = 1.0f / sqrtf((float)D.head_dim);
     a.out = s->attn; a.scratch = s->att_scratch; a.tickets = s->att_tickets;
-    a.run_state = s->run_state; a.run_state_w = s->run_state;
-    a.cancel_word = nullptr; a.run_id = run_id; a.err = s->err;  // see O-proj
-    SP_CHECK(launch_attention(a, D.w_dtype, D.head_dim, st));
-    // x += attn @ Wo (model.py:416)
-    g = sp_gemv_args{};
-    g.w_dtype = D.w_dtype; g.run_state = s->run_state; g.err = s->err; g.toks = dd;
-    g.m = n; g.w = L.o; g.n_rows = d; g.k = s->q_dim; g.x = s->attn; g.ldx = s->q_dim;
-    g.norm = 0; g.epi = SP_EPI_RESID; g.out = x_out; g.ldo = d;
-    g.cancel_word = cancel_word; g.run_state_w = s->run_state; g.run_id = run_id;
-    rc = sp_gemv(&g, stream);
-    if (rc) return rc;
-    g.cancel_word = nullptr; g.run_state_w = nullptr;
-    // h = act(rmsnorm(x) @ W1) (model.py:417-418)
-    g.w = L.up; g.n_rows = s->up_rows; g.k = d; g.x = x_out; g.ldx = d;
-    g.norm = 1; g.norm_eps = D.norm_eps; g.gain = llama ? L.mlp_norm : nullptr;
-    g.epi = llama ? SP_EPI_SWIGLU : SP_EPI_GELU; g.out = s->h; g.ldo = D.ffn_dim;
-    rc = sp_gemv(&g, stream);
-    if (rc) return rc;
-    // x += h @ W2 (+ finite check, model.py:418-420)
-    g.w = L.down; g.n_rows = d; g.k = D.ffn_dim; g.x = s->h; g.ldx = D.ffn_dim;
-    g.norm = 0; g.gain = nullptr; g.epi = SP_EPI_RESID; g.out = x_out; g.ldo = d;
-    rc = sp_gemv(&g, stream);
-    if (rc) return rc;
+    a.run_state = s->run_state; a.run_state_w = nullptr;
+    a.cancel_word = nullptr; a.run_id = run_id; a.err = s->err;
+    if (s->tc) {
+      // ---- tensor-core path (tcgen05, bf16 activations, fp32 accumulate) ----
+      TcArgs t{};
+      t.m = n; t.toks = dd; t.err = s->err; t.run_state = s->run_state;
+      t.scratch = s->tc_scratch; t.tickets = s->tc_tickets; t.norm_eps = D.norm_eps;
+      t.ss_ld = s->max_tokens;
+      // q, k, v (+RoPE, K/V into the cell rows): model.py:387-393
+      t.n_rows = s->q_dim + 2 * s->kv_dim; t.k = d; t.epi = SP_EPI_QKV; t.norm = 1;
+      t.ss_in = s->ss; t.ss_nparts = ss_parts; t.out = s->q; t.ldo = s->q_dim;
+      t.q_rows = s->q_dim; t.kv_rows = s->kv_dim; t.k_cache = kl; t.v_cache = vl;
+      t.cache_row0 = row0; t.head_dim = D.head_dim; t.rope_theta = D.rope_theta;
+      t.w = L.qkv;
+      SP_CHECK(launch_tc_gemm(s->m_xb, t, st));
+      a.out = reinterpret_cast<float*>(s->attnb); a.out_bf16 = 1;
+      SP_CHECK(launch_attention(a, D.w_dtype, D.head_dim, st));
+      // x += attn @ Wo, emit bf16(x * mlp_norm) and its statistic
+      TcArgs o = t;
+      o.n_rows = d; o.k = s->q_dim; o.epi = SP_EPI_RESID; o.norm = 0; o.out = x_out;
+      o.ldo = d; o.ss_out = s->ss; o.xb_next = s->xb; o.gain_next = L.mlp_norm;
+      o.w = L.o;
+      SP_CHECK(launch_tc_gemm(s->m_attnb, o, st));
+      ss_parts = d / 128;
+      // h = silu(g) * u of rmsnorm(x)
+      TcArgs u = t;
+      u.n_rows = 2 * D.ffn_dim; u.k = d; u.epi = SP_EPI_SWIGLU; u.norm = 1;
+      u.ss_in = s->ss; u.ss_nparts = ss_parts; u.out = s->hb; u.ldo = D.ffn_dim;
+      u.w = L.up;
+      SP_CHECK(launch_tc_gemm(s->m_xb, u, st));
+      // x += h @ Wd (+ finite check), emit the next layer's normed input
+      TcArgs dn = t;
+      dn.n_rows = d; dn.k = D.ffn_dim; dn.epi = SP_EPI_RESID; dn.norm = 0; dn.out = x_out;
+      dn.ldo = d; dn.ss_out = s->ss; dn.xb_next = s->xb;
+      dn.gain_next = (l + 1 < s->hi) ? s->layers[l + 1 - s->lo].attn_norm : nullptr;
+      dn.w = L.down;
+      SP_CHECK(launch_tc_gemm(s->m_hb, dn, st));
+    } else {
+      // ---- CUDA-core path (fp32 ref arch): weight-streaming GEMV ----
+      sp_gemv_args g{};
+      g.w_dtype = D.w_dtype;
+      g.run_state = s->run_state;
+      g.err = s->err;
+      g.toks = dd;
+      g.m = n;
+      // q, k, v (model.py:387-393): rmsnorm fused, k/v into cell rows
+      g.w = L.qkv; g.n_rows = s->q_dim + 2 * s->kv_dim; g.k = d;
+      g.x = x_out; g.ldx = d; g.norm = 1; g.norm_eps = D.norm_eps;
+      g.gain = llama ? L.attn_norm : nullptr;
+      g.epi = SP_EPI_QKV; g.out = s->q; g.ldo = s->q_dim;
+      g.q_rows = s->q_dim; g.kv_rows = s->kv_dim; g.k_cache = kl; g.v_cache = vl;
+      g.cache_row0 = row0; g.rope = llama ? 1 : 0; g.head_dim = D.head_dim;
+      g.rope_theta = D.rope_theta;
+      int rc = sp_gemv(&g, stream);
+      if (rc) return rc;
+      // attention over the plan (model.py:394-415)
+      SP_CHECK(launch_attention(a, D.w_dtype, D.head_dim, st));
+      // x += attn @ Wo (model.py:416)
+      g = sp_gemv_args{};
+      g.w_dtype = D.w_dtype; g.run_state = s->run_state; g.err = s->err; g.toks = dd;
+      g.m = n; g.w = L.o; g.n_rows = d; g.k = s->q_dim; g.x = s->attn; g.ldx = s->q_dim;
+      g.norm = 0; g.epi = SP_EPI_RESID; g.out = x_out; g.ldo = d;
+      rc = sp_gemv(&g, stream);
+      if (rc) return rc;
+      // h = act(rmsnorm(x) @ W1) (model.py:417-418)
+      g.w = L.up; g.n_rows = s->up_rows; g.k = d; g.x = x_out; g.ldx = d;
+      g.norm = 1; g.norm_eps = D.norm_eps; g.gain = llama ? L.mlp_norm : nullptr;
+      g.epi = llama ? SP_EPI_SWIGLU : SP_EPI_GELU; g.out = s->h; g.ldo = D.ffn_dim;
+      rc = sp_gemv(&g, stream);
+      if (rc) return rc;
+      // x += h @ W2 (+ finite check, model.py:418-420)
+      g.w = L.down; g.n_rows = d; g.k = D.ffn_dim; g.x = s->h; g.ldx = D.ffn_dim;
+      g.norm = 0; g.gain = nullptr; g.epi = SP_EPI_RESID; g.out = x_out; g.ldo = d;
+      rc = sp_gemv(&g, stream);
+      if (rc) return rc;
+    }
+    // early inference cancellation: observe the cancel word between layers
+    // (engine.py:602-612 drains cancels between layers)
+    if (cancel_word && l + 1 < layer_b && ((l + 1 - layer_a) % OBSERVE_EVERY) == 0) {
+      SP_CHECK(launch_pdl(observe_kernel, dim3(1), dim3(1), 0, st, cancel_word, run_id,
+                          s->run_state));
+    }
   }
-  epilogue_kernel<<<max(1, min(148, (s->n_cells + 255) / 256)), 256, 0, st>>>(
-      dd, n, s->run_state, s->cell_pos, s->cell_mask, s->n_cells, row0, out_status);
-  SP_CHECK(cudaGetLastError());
+  SP_CHECK(launch_pdl(epilogue_kernel, dim3(max(1, min(148, (s->n_cells + 255) / 256))),
+                      dim3(256), 0, st, (const sp_token*)dd, n, (const int*)s->run_state,
+                      (const int32_t*)s->cell_pos, s->cell_mask, s->n_cells, row0, out_status));
   return SP_OK;
 }
 
@@ -496,8 +630,8 @@ extern "C" int sp_stage_lmhead(sp_stage* s, const float* x,
   for (int i = 0; i < n_rows; ++i) hr[i] = host_rows[i];
   SP_CHECK(cudaMemcpyAsync(dr, hr, sizeof(int32_t) * n_rows, cudaMemcpyHostToDevice, st));
   SP_CHECK(cudaEventRecord(s->ev[k], st));
-  gather_rows_kernel<<<n_rows, 128, 0, st>>>(x, D.d_model, dr, s->xg, s->run_state);
-  SP_CHECK(cudaGetLastError());
+  SP_CHECK(launch_pdl(gather_rows_kernel, dim3(n_rows), dim3(128), 0, st, x, D.d_model,
+                      (const int32_t*)dr, s->xg, (const int*)s->run_state));
   LmArgs a{};
   a.w = s->w_out; a.V = D.vocab; a.d = D.d_model; a.x = s->xg; a.n_rows = n_rows;
   a.norm = 1; a.eps = D.norm_eps;
@@ -704,6 +838,16 @@ extern "C" int sp_lmhead(const void* w_out, int w_dtype, int vocab, int d,
   a.scratch = reinterpret_cast<LmPartial*>(scratch); a.ticket = tickets;
   a.err = err; a.run_state = run_state;
   return cuda_status(launch_lmhead(a, w_dtype, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int sp_tc_gemm(const sp_tc_args* a, const void* x, int x_rows, void* stream) {
+  if (!a || !a->w || !x || a->n_rows % 128 || a->k % 64 || a->m <= 0 || x_rows < 128)
+    return SP_ERR_ARG;
+  CUtensorMap mx[2];
+  if (!make_map_bf16(&mx[0], x, x_rows, a->k, a->k, 16) ||
+      !make_map_bf16(&mx[1], x, x_rows, a->k, a->k, 128))
+    return SP_ERR_CUDA;
+  return cuda_status(launch_tc_gemm(mx, *a, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 extern "C" const char* sp_version(void) { return "specpipe_b200 0.1 sm_100a"; }

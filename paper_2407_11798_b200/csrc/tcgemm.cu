@@ -1,0 +1,500 @@
+// Skinny tensor-core GEMM for the bf16 (llama) decoder path: tcgen05.mma
+// with TMEM accumulators, TMA-fed 4-stage mbarrier pipeline, split-K across
+// CTAs and fused epilogues.  Replaces the CUDA-core GEMV for every llama run
+// (single-token, speculative verification and prefill alike), so a token's
+// result does not depend on how many tokens share the launch.
+//
+//   D[128 rows, NT tokens] += W[128 rows, 64 k] . X[NT tokens, 64 k]^T
+//
+// swap-AB: the weight tile is the A operand (UMMA_M = 128, K-major, SW128),
+// the activation tile the B operand (UMMA_N = NT, K-major, SW128).  The
+// CTA's K range is split into 64-element chunks; warp 0 lane 0 streams
+// W and X chunks with cp.async.bulk.tensor into a ring of stages, warp 1
+// lane 0 issues 4 UMMA_K=16 MMAs per chunk and commits each stage back to
+// its "empty" barrier.  With ksplit > 1 each CTA parks its fp32 partial in
+// global scratch and the last-arriving CTA of a row tile sums the splits in
+// ascending order (deterministic) and runs the epilogue.
+//
+// Reference sites of the fused epilogues: model.py:387-393 (q,k,v + cache
+// insert), 416 (out-proj residual), 417-418 (MLP, SwiGLU in the llama
+// variant), 419-420 (finite check); RMSNorm (model.py:188-189) is applied
+// as a per-token scale from the producer's sum-of-squares partials.
+#include <cuda.h>
+
+#include "gemv_core.cuh"
+#include "kernels.cuh"
+
+namespace sp {
+
+constexpr int TC_THREADS = 128;
+constexpr int TC_STAGES = 4;
+constexpr int TC_BM = 128;     // weight rows per tile (UMMA_M)
+constexpr int TC_BK = 64;      // K elements per chunk (one 128B swizzle atom)
+constexpr int TC_WTILE = TC_BM * TC_BK * 2;
+
+// ---- PTX wrappers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity), "r"(1000u)
+      : "memory");
+  return ok != 0;
+}
+// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  for (uint32_t it = 0; !mbar_try(b, parity); ++it)
+    if (it > (1u << 22)) __trap();
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+// 1D bulk copy global -> shared, completing on an mbarrier (weights are
+// stored pre-tiled and pre-swizzled: one [128 x 64] bf16 tile = 16 KB).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// K-major, 128B-swizzled smem descriptor (canonical atom: 8 rows x 128 B,
+// 8-row groups 1024 B apart); sm_100 descriptor version 1.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+  d |= (uint64_t)1 << 16;                         // LBO (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;               // SBO: 8-row group stride
+  d |= (uint64_t)1 << 46;                         // version = 1 (sm_100)
+  d |= (uint64_t)2 << 61;                         // layout: SWIZZLE_128B
+  return d;
+}
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// 32 lanes x 32-bit, 16 consecutive columns per thread (its TMEM lane).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcSmemTail {
+  uint64_t full[TC_STAGES];
+  uint64_t empty[TC_STAGES];
+  uint64_t done;
+  uint32_t tmem_base;
+  int last;
+  float inv_rms[128];
+  float ssw[4][128];
+};
+
+// ---- the kernel -------------------------------------------------------------
+template <int NT, int EPI, bool NORM>
+__global__ void __launch_bounds__(TC_THREADS)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
+  constexpr int XTILE = NT * TC_BK * 2;
+  constexpr int STAGE = TC_WTILE + XTILE;
+  constexpr uint32_t TMEM_COLS = NT < 32 ? 32 : NT;
+  extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  TcSmemTail* tail = reinterpret_cast<TcSmemTail*>(smem + TC_STAGES * STAGE);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, split = blockIdx.y, nsplit = gridDim.y;
+  const int nchunk = a.k / TC_BK;
+  const int c0 = (int)((long)nchunk * split / nsplit);
+  const int c1 = (int)((long)nchunk * (split + 1) / nsplit);
+  const int nloc = c1 - c0;
+  const int npre = nloc < TC_STAGES ? nloc : TC_STAGES;
+  // this CTA's weight tiles [tile][c0..c1) are one contiguous run
+  const __nv_bfloat16* wtiles =
+      reinterpret_cast<const __nv_bfloat16*>(a.w) + (size_t)tile * nchunk * (TC_WTILE / 2);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&tail->full[s], 1);
+      mbar_init(&tail->empty[s], 1);
+    }
+    mbar_init(&tail->done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    // Weights do not depend on the previous kernel: start streaming the
+    // first stages before the programmatic dependency is resolved.
+    const uint64_t pw = policy_evict_first();
+    for (int i = 0; i < npre; ++i) {
+      mbar_expect_tx_only(&tail->full[i], TC_WTILE);
+      bulk_load(smem + i * STAGE, wtiles + (size_t)(c0 + i) * (TC_WTILE / 2), TC_WTILE,
+                &tail->full[i], pw);
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tail->tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tail->tmem_base;
+
+  // ---- programmatic dependency: everything below may read the previous
+  // kernel's outputs (activations, run_state, norm statistics)
+  pdl_wait();
+  pdl_trigger();
+  if (run_skipped(a.run_state)) {        // consistent for the whole grid
+    if (threadIdx.x == 0) {              // drain the weight prefetch
+      for (int i = 0; i < npre; ++i) {
+        mbar_arrive(&tail->full[i]);
+        mbar_wait(&tail->full[i], 0);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS));
+    return;
+  }
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+    for (int i = 0; i < nloc; ++i) {
+      const int s = i % TC_STAGES;
+      const uint32_t ph = (i / TC_STAGES) & 1;
+      uint8_t* st = smem + s * STAGE;
+      if (i < npre) {                    // weights already in flight
+        mbar_expect_tx(&tail->full[s], XTILE);
+      } else {
+        mbar_wait(&tail->empty[s], ph ^ 1);
+        mbar_expect_tx(&tail->full[s], STAGE);
+        bulk_load(st, wtiles + (size_t)(c0 + i) * (TC_WTILE / 2), TC_WTILE, &tail->full[s], pw);
+      }
+      tma_load_2d(st + TC_WTILE, &tmX, &tail->full[s], (c0 + i) * TC_BK, a.tok0, px);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    constexpr uint32_t IDESC = idesc_bf16(TC_BM, NT);
+    for (int i = 0; i < nloc; ++i) {
+      const int s = i % TC_STAGES;
+      const uint32_t ph = (i / TC_STAGES) & 1;
+      mbar_wait(&tail->full[s], ph);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * STAGE);
+      const uint32_t sb = sa + TC_WTILE;
+#pragma unroll
+      for (int k = 0; k < TC_BK / 16; ++k)
+        umma_bf16(tmem, umma_desc_sw128(sa + 32 * k), umma_desc_sw128(sb + 32 * k), IDESC,
+                  (i > 0 || k > 0) ? 1u : 0u);
+      umma_commit(&tail->empty[s]);
+    }
+    umma_commit(&tail->done);
+  }
+
+  // ---- epilogue: TMEM -> registers (thread = weight row, NT token columns)
+  mbar_wait(&tail->done, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;          // row within the tile
+  const int R = tile * TC_BM + row;          // global weight row
+  const int mv = min(NT, a.m - a.tok0);
+  float acc[NT];
+  if (nloc > 0) {
+#pragma unroll
+    for (int c = 0; c < NT; c += 16)
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c, acc + c);
+  } else {
+#pragma unroll
+    for (int c = 0; c < NT; ++c) acc[c] = 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+
+  if (nsplit > 1) {
+    // park the partial; the last CTA of this row tile merges in split order
+    float* part = a.scratch + ((size_t)tile * nsplit + split) * NT * TC_BM;
+#pragma unroll
+    for (int c = 0; c < NT; ++c) part[c * TC_BM + row] = acc[c];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      tail->last = (atomicAdd(&a.tickets[tile], 1) == nsplit - 1);
+    __syncthreads();
+    if (!tail->last) return;
+    __threadfence();
+    const float* base = a.scratch + (size_t)tile * nsplit * NT * TC_BM;
+#pragma unroll
+    for (int c = 0; c < NT; ++c) acc[c] = ld_volatile_f(base + c * TC_BM + row);
+    for (int sp2 = 1; sp2 < nsplit; ++sp2) {
+      const float* p = base + (size_t)sp2 * NT * TC_BM;
+#pragma unroll
+      for (int c = 0; c < NT; ++c) acc[c] = __fadd_rn(acc[c], ld_volatile_f(p + c * TC_BM + row));
+    }
+    if (threadIdx.x == 0) a.tickets[tile] = 0;
+  }
+
+  // per-token RMSNorm scale from the producer's sum-of-squares partials
+  if (NORM) {
+    if (threadIdx.x < mv) {
+      const int t = a.tok0 + threadIdx.x;
+      float s = 0.f;
+      for (int p = 0; p < a.ss_nparts; ++p) s = __fadd_rn(s, a.ss_in[(size_t)p * a.ss_ld + t]);
+      tail->inv_rms[threadIdx.x] = rms_scale(s, a.k, a.norm_eps);
+    }
+    __syncthreads();
+  }
+
+  if (EPI == SP_EPI_QKV) {
+    const int hd = a.head_dim;
+    int sec, off;
+    if (R < a.q_rows) { sec = 0; off = R; }
+    else if (R < a.q_rows + a.kv_rows) { sec = 1; off = R - a.q_rows; }
+    else { sec = 2; off = R - a.q_rows - a.kv_rows; }
+    const bool odd = (R & 1) != 0;
+    int dim = off;
+    float inv = 0.f;
+    if (sec < 2) {                         // RoPE pair (j, j + hd/2) on rows (2j, 2j+1)
+      const int head = off / hd, j = (off % hd) >> 1;
+      dim = head * hd + j + (odd ? (hd >> 1) : 0);
+      inv = powf(a.rope_theta, -2.0f * (float)j / (float)hd);
+    }
+#pragma unroll
+    for (int c = 0; c < NT; ++c) {
+      float y = acc[c];
+      if (NORM) y = __fmul_rn(y, c < mv ? tail->inv_rms[c] : 0.f);
+      const float partner = __shfl_xor_sync(0xffffffffu, y, 1);
+      if (c >= mv) continue;
+      const int t = a.tok0 + c;
+      float o = y;
+      if (sec < 2) {
+        float sn, cs;
+        sincosf((float)a.toks[t].pos * inv, &sn, &cs);
+        o = odd ? (y * cs + partner * sn) : (y * cs - partner * sn);
+      }
+      if (sec == 0) {
+        reinterpret_cast<float*>(a.out)[(size_t)t * a.ldo + dim] = o;
+      } else {
+        __nv_bfloat16* cache = reinterpret_cast<__nv_bfloat16*>(sec == 1 ? a.k_cache : a.v_cache);
+        cache[(size_t)(a.cache_row0 + t) * a.kv_rows + dim] = __float2bfloat16_rn(o);
+      }
+    }
+  } else if (EPI == SP_EPI_SWIGLU) {
+    const bool odd = (R & 1) != 0;
+#pragma unroll
+    for (int c = 0; c < NT; ++c) {
+      float y = acc[c];
+      if (NORM) y = __fmul_rn(y, c < mv ? tail->inv_rms[c] : 0.f);
+      const float up = __shfl_xor_sync(0xffffffffu, y, 1);
+      if (c >= mv || odd) continue;
+      const int t = a.tok0 + c;
+      reinterpret_cast<__nv_bfloat16*>(a.out)[(size_t)t * a.ldo + (R >> 1)] =
+          __float2bfloat16_rn(__fmul_rn(silu(y), up));
+    }
+  } else if (EPI == SP_EPI_RESID) {
+    float* x = reinterpret_cast<float*>(a.out);
+    const float g = a.gain_next ? a.gain_next[R] : 1.0f;
+    float sq[NT];
+#pragma unroll
+    for (int c = 0; c < NT; ++c) {
+      sq[c] = 0.f;
+      if (c < mv) {
+        const int t = a.tok0 + c;
+        float* xp = x + (size_t)t * a.ldo + R;
+        const float nv = __fadd_rn(*xp, acc[c]);
+        *xp = nv;
+        if (!isfinite(nv)) set_error(a.err, SP_DEV_NONFINITE);
+        if (a.xb_next)
+          reinterpret_cast<__nv_bfloat16*>(a.xb_next)[(size_t)t * a.ldo + R] =
+              __float2bfloat16_rn(__fmul_rn(nv, g));
+        sq[c] = __fmul_rn(nv, nv);
+      }
+    }
+    // per-token sum of squares of this tile's 128 rows (fixed order)
+#pragma unroll
+    for (int c = 0; c < NT; ++c) {
+      const float s = warp_sum(sq[c]);
+      if (lane == 0) tail->ssw[warp][c] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < mv) {
+      const int c = threadIdx.x;
+      const float s = __fadd_rn(__fadd_rn(tail->ssw[0][c], tail->ssw[1][c]),
+                                __fadd_rn(tail->ssw[2][c], tail->ssw[3][c]));
+      a.ss_out[(size_t)tile * a.ss_ld + a.tok0 + c] = s;
+    }
+  } else {  // SP_EPI_STORE
+#pragma unroll
+    for (int c = 0; c < mv; ++c) {
+      float y = acc[c];
+      if (NORM) y = __fmul_rn(y, tail->inv_rms[c]);
+      reinterpret_cast<float*>(a.out)[(size_t)(a.tok0 + c) * a.ldo + R] = y;
+    }
+  }
+}
+
+// ---- host side --------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2D bf16 map over a row-major [rows, cols] matrix (cols contiguous) with a
+// {64, box_rows} box and 128B swizzle.
+bool make_map_bf16(CUtensorMap* map, const void* base, long rows, long cols, long ld_elems,
+                   int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld_elems * 2};
+  cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+template <int NT, int EPI, bool NORM>
+static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
+                             cudaStream_t st) {
+  constexpr int STAGE = TC_WTILE + NT * TC_BK * 2;
+  const int smem = TC_STAGES * STAGE + (int)sizeof(TcSmemTail) + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tc_gemm_kernel<NT, EPI, NORM>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  dim3 grid(a.n_rows / TC_BM, ksplit);
+  return launch_pdl(tc_gemm_kernel<NT, EPI, NORM>, grid, dim3(TC_THREADS), smem, st, x, a);
+}
+
+template <int NT>
+static cudaError_t launch_epi(const CUtensorMap& x, const TcArgs& a, int ksplit,
+                              cudaStream_t st) {
+  switch (a.epi) {
+    case SP_EPI_QKV:
+      return a.norm ? launch_nt<NT, SP_EPI_QKV, true>(x, a, ksplit, st)
+                    : launch_nt<NT, SP_EPI_QKV, false>(x, a, ksplit, st);
+    case SP_EPI_SWIGLU:
+      return a.norm ? launch_nt<NT, SP_EPI_SWIGLU, true>(x, a, ksplit, st)
+                    : launch_nt<NT, SP_EPI_SWIGLU, false>(x, a, ksplit, st);
+    case SP_EPI_RESID:
+      return launch_nt<NT, SP_EPI_RESID, false>(x, a, ksplit, st);
+    case SP_EPI_STORE:
+      return a.norm ? launch_nt<NT, SP_EPI_STORE, true>(x, a, ksplit, st)
+                    : launch_nt<NT, SP_EPI_STORE, false>(x, a, ksplit, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int tc_nt_for(int m) { return m <= 16 ? 16 : 128; }
+
+// Split-K factor: as many CTAs as fit in ONE wave (a second partial wave
+// doubles the tail) but at least 16 chunks (256 KB of weights) per CTA so
+// the fixed prologue/merge cost is amortised (measured on the 7B shapes:
+// QKV 3, O 4, gate/up 1, down 9).
+int tc_ksplit(int n_rows, int k, int target_ctas) {
+  const int tiles = n_rows / TC_BM, nchunk = k / TC_BK;
+  return max(1, min(target_ctas / tiles, nchunk / 16));
+}
+
+// Launch over all tokens (token tiles of NT); maps[0] is the NT=16 X map,
+// maps[1] the NT=128 one.
+cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st) {
+  const int nt = tc_nt_for(a.m);
+  const int ksplit = a.ksplit > 0 ? a.ksplit : tc_ksplit(a.n_rows, a.k, 2 * 148);
+  for (int t0 = 0; t0 < a.m; t0 += nt) {
+    a.tok0 = t0;
+    cudaError_t e = nt == 16 ? launch_epi<16>(xmaps[0], a, ksplit, st)
+                             : launch_epi<128>(xmaps[1], a, ksplit, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace sp

@@ -225,6 +225,7 @@ class DeviceModel:
         self.final_norm = None    # [d] fp32 (llama)
         self.layers = {}          # layer -> dict of device tensors
         self.host = None
+        self.tiled = config.arch == "llama"    # tensor-core weight layout
         self._head_stage = None
 
     @property
@@ -256,8 +257,10 @@ class DeviceModel:
         out["w_out"] = None if self.w_out is None else f64(self.w_out).T.copy()
         out["final_norm"] = None if self.final_norm is None else f64(self.final_norm)
         lo, hi = self.layer_range
+        lay = (lambda t: untile_weight(t)) if self.tiled else (lambda t: t)
         for l in range(lo, hi):
-            L = self.layers[l]
+            L = {k: (lay(v) if k in ("qkv", "o", "up", "down") else v)
+                 for k, v in self.layers[l].items()}
             qkv = f64(L["qkv"])
             q, k, v = qkv[:H * hd], qkv[H * hd:H * hd + KH * hd], qkv[H * hd + KH * hd:]
             if cfg.arch == "llama":
@@ -272,6 +275,35 @@ class DeviceModel:
                 d["w1"], d["w2"] = up.T.copy(), f64(L["down"]).T.copy()
             out["layers"].append(d)
         return out
+
+
+def _swizzle_gather(t):
+    """Within each 128x64 tile, 16-byte chunk p of row r holds logical chunk
+    p ^ (r % 8) (the 128B swizzle); XOR is an involution, so the same gather
+    both applies and removes it.  ``t``: [Tr, Tc, 128, 8, 8]."""
+    import torch
+    r = torch.arange(128, device=t.device).view(128, 1)
+    j = torch.arange(8, device=t.device).view(1, 8)
+    idx = (j ^ (r % 8)).view(1, 1, 128, 8, 1).expand(t.shape)
+    return torch.gather(t, 3, idx)
+
+
+def tile_weight(w):
+    """Row-major [N, K] bf16 -> the tensor-core layout: [N/128][K/64] tiles
+    of 128 x 64, each the 128B-swizzled K-major image a UMMA descriptor
+    reads, so one tile is one contiguous 16 KB bulk copy and a CTA's K range
+    is one sequential run of HBM (tcgemm.cu)."""
+    N, K = w.shape
+    if N % 128 or K % 64:
+        raise ModelError(f"tensor-core weights need N % 128 == 0 and K % 64 == 0, got {N}x{K}")
+    t = w.reshape(N // 128, 128, K // 64, 8, 8).permute(0, 2, 1, 3, 4)
+    return _swizzle_gather(t).contiguous().reshape(N, K)
+
+
+def untile_weight(w):
+    N, K = w.shape
+    t = _swizzle_gather(w.reshape(N // 128, K // 64, 128, 8, 8))
+    return t.permute(0, 2, 1, 3, 4).contiguous().reshape(N, K)
 
 
 def permute_rope_rows(w: np.ndarray, n_heads: int, hd: int):
@@ -392,9 +424,10 @@ def build_model(config: ModelConfig, device=None, layer_range=None,
         up[0::2] = wg
         up[1::2] = wu
         del wg, wu
-        m.layers[l] = dict(qkv=torch.cat([wq, wk, wv], 0).contiguous(), o=wo,
-                           up=up, down=wd, attn_norm=ones.clone(),
+        m.layers[l] = dict(qkv=tile_weight(torch.cat([wq, wk, wv], 0)), o=tile_weight(wo),
+                           up=tile_weight(up), down=tile_weight(wd), attn_norm=ones.clone(),
                            mlp_norm=ones.clone())
+        del wq, wk, wv, wo, up, wd
     if want_head:
         m.w_out = draw(1, (config.vocab_size, d), 1 / math.sqrt(d))
         m.final_norm = ones.clone()

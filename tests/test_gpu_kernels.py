@@ -121,3 +121,104 @@ def test_lmhead_top2_conf(env):
             conf = o[i, 2:3].view(np.float32)[0]
             e = np.exp(v - v.max())
             assert abs(conf - e.max() / e.sum()) < 1e-5
+
+
+# ---------------------------------------------------------------------------
+# tcgen05 skinny GEMM (bf16 path)
+# ---------------------------------------------------------------------------
+
+def _tc(env, W, X, epi=0, m=None, norm=False, ss=None, ksplit=0, out=None, ldo=None,
+        **kw):
+    torch, _lib, lib = env
+    n, k = W.shape
+    m = X.shape[0] if m is None else m
+    from paper_2407_11798_b200.model import tile_weight, untile_weight
+    Wd = torch.from_numpy(W.astype(np.float32)).to("cuda", torch.bfloat16).contiguous()
+    Wt = tile_weight(Wd)
+    assert torch.equal(untile_weight(Wt), Wd)
+    xr = max(128, X.shape[0])
+    Xd = torch.zeros((xr, k), dtype=torch.bfloat16, device="cuda")
+    Xd[:X.shape[0]] = torch.from_numpy(X.astype(np.float32)).to("cuda", torch.bfloat16)
+    if out is None:
+        out = torch.zeros((m, n if ldo is None else ldo), dtype=torch.float32, device="cuda")
+    scratch = torch.zeros(8 << 20, dtype=torch.float32, device="cuda")
+    tick = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    a = _lib.sp_tc_args()
+    a.w = Wt.data_ptr()
+    a.n_rows, a.k, a.m, a.epi, a.norm, a.norm_eps = n, k, m, epi, int(norm), 1e-5
+    a.out, a.ldo = out.data_ptr(), out.shape[1]
+    a.scratch, a.tickets, a.err, a.ksplit = scratch.data_ptr(), tick.data_ptr(), err.data_ptr(), ksplit
+    keep = []
+    if ss is not None:
+        ssd = torch.from_numpy(ss.astype(np.float32)).cuda().contiguous()
+        keep.append(ssd)
+        a.ss_in, a.ss_nparts, a.ss_ld = ssd.data_ptr(), ss.shape[0], ss.shape[1]
+    for key, v in kw.items():
+        if hasattr(v, "data_ptr"):
+            keep.append(v)
+            v = v.data_ptr()
+        setattr(a, key, v)
+    _lib.check(lib.sp_tc_gemm(C.byref(a), Xd.data_ptr(), xr,
+                              torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    Wq = Wd.float().cpu().numpy().astype(np.float64)
+    Xq = Xd[:X.shape[0]].float().cpu().numpy().astype(np.float64)
+    return out, Wq, Xq, tick
+
+
+@pytest.mark.parametrize("m", [1, 3, 5, 16, 17, 128, 130])
+@pytest.mark.parametrize("shape", [(128, 64), (256, 768), (4096, 4096), (384, 11008)])
+def test_tc_gemm_store(env, m, shape):
+    n, k = shape
+    r = np.random.default_rng(n + k + m)
+    W = r.standard_normal((n, k)) / np.sqrt(k)
+    X = r.standard_normal((m, k))
+    out, Wq, Xq, tick = _tc(env, W, X)
+    ref = Xq @ Wq.T
+    got = out.cpu().numpy()
+    assert np.abs(got - ref).max() < 2e-3 * max(1.0, np.abs(ref).max()), np.abs(got - ref).max()
+    assert int(tick.abs().sum()) == 0          # split-K tickets reset
+
+
+def test_tc_gemm_norm_and_ksplit_invariance(env):
+    r = np.random.default_rng(1)
+    n, k, m = 512, 4096, 4
+    W = r.standard_normal((n, k)) / np.sqrt(k)
+    X = r.standard_normal((m, k))
+    ss = np.stack([np.full(m, 0.0), (X * X).sum(1)])   # 2 partials summing to the stat
+    outs = []
+    for ks in (1, 3, 7):
+        out, Wq, Xq, _ = _tc(env, W, X, norm=True, ss=ss, ksplit=ks)
+        outs.append(out.cpu().numpy())
+    inv = 1 / np.sqrt(ss.sum(0) / k + 1e-5)
+    ref = (Xq @ Wq.T) * inv[:, None]
+    for o in outs:
+        assert np.abs(o - ref).max() < 2e-3
+    # a token's result does not depend on the batch it shares the launch with
+    o1, _, _, _ = _tc(env, W, X[:1], norm=True, ss=ss[:, :1], ksplit=3)
+    assert np.array_equal(o1.cpu().numpy()[0], outs[1][0])
+
+
+def test_tc_gemm_resid_swiglu(env):
+    torch = env[0]
+    r = np.random.default_rng(2)
+    n, k, m = 256, 1024, 3
+    W = r.standard_normal((n, k)) / np.sqrt(k)
+    X = r.standard_normal((m, k))
+    base = r.standard_normal((m, n)).astype(np.float32)
+    g = (1 + 0.1 * r.standard_normal(n)).astype(np.float32)
+    x = torch.from_numpy(base.copy()).cuda()
+    xb = torch.zeros((m, n), dtype=torch.bfloat16, device="cuda")
+    ssout = torch.zeros((n // 128, m), dtype=torch.float32, device="cuda")
+    out, Wq, Xq, _ = _tc(env, W, X, epi=1, out=x, xb_next=xb,
+                         gain_next=torch.from_numpy(g).cuda(), ss_out=ssout, ss_ld=m)
+    new = base + Xq @ Wq.T
+    assert np.abs(x.cpu().numpy() - new).max() < 2e-3
+    assert np.abs(xb.float().cpu().numpy() - new * g).max() < 2e-2
+    assert np.abs(ssout.cpu().numpy().sum(0) - (new * new).sum(1)).max() < 1e-2
+    hb = torch.zeros((m, n // 2), dtype=torch.bfloat16, device="cuda")
+    _tc(env, W, X, epi=4, out=hb)
+    z = Xq @ Wq.T
+    sw = z[:, 0::2] / (1 + np.exp(-z[:, 0::2])) * z[:, 1::2]
+    assert np.abs(hb.float().cpu().numpy() - sw).max() < 2e-2
