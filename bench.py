@@ -193,9 +193,10 @@ def gemv_roofline(engine, reps: int = 5) -> dict:
     times = []
     for rep in range(reps + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        graph.replay()
-        e1.record(s)
+        with torch.cuda.stream(s):     # replay() launches on the current stream
+            e0.record(s)
+            graph.replay()
+            e1.record(s)
         e1.synchronize()
         if rep:
             times.append(e0.elapsed_time(e1) / 1e3)

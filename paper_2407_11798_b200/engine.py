@@ -94,6 +94,8 @@ class ExperimentConfig:
     draft_shape: Optional[str] = None    # e.g. "llama-160m"
     capacity: int = 8192                 # cell pool per stage
     max_run_tokens: int = 256            # largest batch (prefill) per stage-run
+    draft_charge: bool = True            # synthetic draft pays a real draft forward
+                                         # per token (False ~ draft_token_delay=0)
 
     def validate(self) -> None:
         if self.mode not in MODES:
@@ -869,7 +871,8 @@ class Engine:
             srv = TableDraftServer(self.draft_model, truth, runner, cfg.alpha, seed,
                                    stream=self._draft_stream,
                                    capacity=min(cfg.capacity, 16 * cfg.max_context),
-                                   stage=None if prev is None else prev.stage)
+                                   stage=None if prev is None else prev.stage,
+                                   charge=cfg.draft_charge)
             if prev is not None:
                 srv.forwards = 0
             self._table_draft = srv

@@ -28,10 +28,13 @@ def cfg(sp, **kw):
 
 
 # Speculation only pays when a draft request is cheaper than a target run.
-# The reference's tests get that from their simulated delays; on the GPU
-# tiny models are launch-bound, so these tests use a deep target and a
-# one-layer draft to make the draft genuinely faster.
-DEEP = dict(target_layers=24, draft_layers=1)
+# The reference's tests get that from their simulated delays.  On the GPU a
+# tiny target is host-bound (the head finds every run already finished, and
+# LOGITS take priority over new draft requests, engine.py:976-989), so these
+# tests use a GPU-bound target (48 llama layers at d=1024, ~1 ms per run) and
+# an uncharged synthetic draft (the analogue of draft_token_delay = 0).
+DEEP = dict(arch="llama", vocab_size=512, embed_dim=1024, n_heads=8, target_layers=48,
+            draft_layers=1, draft_embed_dim=128, draft_charge=False)
 
 
 def deep(sp, **kw):
