@@ -300,6 +300,10 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
         "itl_ms": round(itl * 1e3, 3),
         "acceptance_rate": round(statistics.mean(r.metrics.acceptance_rate for r in res), 4),
         "cancelled_runs_per_step": round(statistics.mean(r.metrics.cancelled_runs for r in res), 1),
+        "runs_per_step": round(statistics.mean(r.metrics.runs_started for r in res), 1),
+        "inflight_mean": round(statistics.mean(r.metrics.inflight_mean for r in res), 2),
+        "head_host_s_per_step": {k: round(statistics.mean(r.host_profile.get(k, 0.0) for r in res), 4)
+                                 for k in ("completion", "reply+spec_launch", "draft_request", "wait")},
         "sync_speculative_tokens_per_s": round(sync_speed, 2),
         "pipeline_iterative_tokens_per_s": round(it_speed, 2),
         "async_over_sync": round(value / sync_speed, 3),

@@ -280,6 +280,7 @@ class SimResult:
     consumed: Dict[Tuple[int, str], int]
     sent: Dict[Tuple[int, str], int]
     records: List[RunRecord]
+    host_profile: Dict[str, float] = field(default_factory=dict)
 
 
 def token_checksum(tokens: Sequence) -> str:
@@ -349,6 +350,8 @@ class Head:
         self.msgs: Dict[Tuple[int, str], int] = {}
         self.stage_logs: Dict[int, list] = {i + 1: [] for i in range(pipe.n_stages)}
         self.tips: Optional[list] = None   # NS-run tips (truth tables)
+        from collections import defaultdict
+        self.profile: Dict[str, float] = defaultdict(float)   # host seconds by activity
         self._t0 = time.perf_counter()
 
     def now(self) -> float:
@@ -565,17 +568,24 @@ class Head:
         self._prefill()
         if not (self.generated >= self.cfg.gen_len or self.terminal):
             self._launch_ns(self.accepted[-1], with_copy=True)
+        prof = self.profile
+        clk = time.perf_counter
         while self.generated < self.cfg.gen_len and not self.terminal:
+            t0 = clk()
             if self.pipe.ready():
                 self._handle_completion(self.pipe.poll())
+                prof["completion"] += clk() - t0
                 continue
             if self.draft_busy and self.draft.ready():
                 self._handle_reply(*self._draft_reply())
+                prof["reply+spec_launch"] += clk() - t0
                 continue
             if not self.draft_busy and self._want_speculation():
                 self._send_draft_request()
+                prof["draft_request"] += clk() - t0
                 continue
             self._block_until_message()
+            prof["wait"] += clk() - t0
         self._finish()
 
     def _block_until_message(self) -> None:
@@ -909,7 +919,8 @@ class Engine:
                          accepted_full=list(head.accepted),
                          accept_events=list(head.accept_events),
                          cancel_log=list(head.cancel_log), node_logs=node_logs,
-                         consumed=dict(sent), sent=sent, records=list(head.records))
+                         consumed=dict(sent), sent=sent, records=list(head.records),
+                         host_profile=dict(head.profile))
 
     def truth(self, prompt: List[int], n: int):
         """Greedy stream and runner-ups of the target along the true path,
