@@ -61,9 +61,11 @@ enum { SP_STATUS_VALID = 0, SP_STATUS_PLACEHOLDER = 1 };
 enum {
   SP_FWD_CHECK_COVERAGE = 1,  /* chain batches: token at pos p sees p cells */
   SP_FWD_SKIPPABLE = 2,       /* speculative: honour cancel / placeholder  */
-  SP_FWD_CONTINUE = 4         /* same run, next layer sub-range: reuse the
+  SP_FWD_CONTINUE = 4,        /* same run, next layer sub-range: reuse the
                                  descriptor, cells and plan (split
                                  evaluation, model.py:5-11)               */
+  SP_FWD_CHAIN = 8            /* draft chain step: token 0 = tip argmax,
+                                 gated by the chain gate                  */
 };
 
 /* Model shape (ModelConfig, model.py:39-64, extended with the llama arch). */
@@ -80,7 +82,12 @@ typedef struct sp_model_dims {
   int32_t w_dtype;     /* SP_DTYPE_* of weights and KV cache            */
   float norm_eps;      /* ref: 1e-8 inside the mean; llama: 1e-5         */
   float rope_theta;
+  int32_t w_layout;    /* SP_LAYOUT_*: bf16 llama stages with TC-tiled
+                          weights run on tcgen05, natural ones on the
+                          CUDA-core GEMV (latency-bound drafts)          */
 } sp_model_dims;
+
+enum { SP_LAYOUT_NATURAL = 0, SP_LAYOUT_TC_TILED = 1 };
 
 /* One BatchToken (model.py:67-75); seq sets are bitmasks (P <= 32). */
 typedef struct sp_token {
@@ -148,6 +155,7 @@ typedef struct sp_gemv_args {
   int* run_state_w;
   const int* cancel_word;
   int32_t run_id;
+  const int32_t* cache_row0_dev;  /* if set, overrides cache_row0 (run header) */
 } sp_gemv_args;
 
 int sp_gemv(const sp_gemv_args* a, void* stream);
@@ -187,8 +195,12 @@ typedef struct sp_tc_args {
   float* scratch;          /* split-K partials                              */
   int* tickets;            /* per row tile, zero-initialised                */
   int32_t ksplit;          /* 0 = auto                                      */
+  int32_t max_ctas;        /* CTA budget for auto split-K (0 = 2 per SM);
+                              a smaller budget leaves SMs free for a
+                              co-scheduled stream (the draft)              */
   int* err;
   const int* run_state;
+  const int32_t* cache_row0_dev;  /* if set, overrides cache_row0 (run header) */
 } sp_tc_args;
 
 /* Low-level form (tests): a->w tiled bf16; X bf16 [x_rows, k] row-major
@@ -245,6 +257,8 @@ int sp_stage_set_layer(sp_stage* s, int layer, const void* w_qkv,
 int sp_stage_set_head(sp_stage* s, const void* w_out, const float* final_norm);
 /* device-visible cancel words: table[run_id % size] == run_id => cancelled */
 int sp_stage_set_cancel_table(sp_stage* s, const int* table, int size);
+/* CTA budget of this stage's tensor-core GEMMs (0 = whole GPU). */
+int sp_stage_set_cta_budget(sp_stage* s, int ctas);
 
 /* Enqueue layers [lo,hi) for one run.  ``host_toks`` is copied into a
  * stream-ordered device descriptor (RUN_CONFIG, engine.py:231-251).
@@ -274,6 +288,42 @@ int sp_stage_lmhead(sp_stage* s, const float* x, const int32_t* host_rows,
                     int n_rows, sp_row_result* out, float* logits_out,
                     int* err_out, int update_tip, int chain_gate, float cutoff,
                     void* stream);
+
+/* One decode / verification stage-run (+ the fused LM head when n_rows > 0)
+ * replayed from a per-shape CUDA graph: every per-run scalar travels in one
+ * small H2D header copy.  Inputs: x_in/in_status (device, NULL on layer 0;
+ * pointers are part of the graph key, so pass fixed buffers); outputs land in
+ * the stage's fixed buffers (sp_stage_io): activations + status word at
+ * x_out[n*d], result block [status, err, -, -] + n_rows sp_row_result.
+ * ``res_copy``: optional destination (device or pinned host) for the result
+ * block.  head_flags: SP_STEP_TIP (remember the tip), SP_STEP_CHAIN (draft
+ * chain step: token 0 = tip argmax, gated; gate &= conf >= cutoff). */
+enum { SP_STEP_TIP = 1, SP_STEP_CHAIN = 2 };
+int sp_stage_step(sp_stage* s, const sp_token* host_toks, int n, int run_id, int kind,
+                  int flags, const int32_t* host_rows, int n_rows, int head_flags,
+                  float cutoff, const float* x_in, const int* in_status, void* res_copy,
+                  void* stream);
+int sp_stage_io(sp_stage* s, float** x_out, sp_row_result** res);
+
+/* A whole draft request as ONE persistent cooperative kernel (K15): feed
+ * n_feed <= 4 tokens at positions pos0.. (their forward + LM head on the
+ * last -> out[0]; with n_feed == 0, out[0] = the current tip), then `steps`
+ * single-token forwards, step j (1-based) -> out[j].  step_tokens == NULL:
+ * chain mode (token = previous argmax; stops once conf < cutoff, remaining
+ * cells dead, like sp_stage_step with SP_STEP_CHAIN); else the given tokens.
+ * Requires a llama bf16 stage with natural-layout weights holding every
+ * layer + head, one sequence, rows == positions (pos0 == n_cells; see
+ * sp_stage_truncate).  Appends n_feed + steps cells.  Replaces the draft
+ * node's per-token loop (engine.py:640-688, speculation.py:142-195). */
+int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_feed, int pos0,
+                          const int32_t* step_tokens, int steps, float cutoff,
+                          sp_row_result* out, int* err_out, void* stream);
+/* Position-addressed stages: drop rows >= n_cells (they are rewritten by the
+ * next tokens; the draft's truncate, kvcache.py:120-149 for one sequence). */
+int sp_stage_truncate(sp_stage* s, int n_cells);
+/* Diagnostics (env SP_DRAFT_PROF=1): %globaltimer stamps of CTA 0 at every
+ * phase edge of the last decode_chain; returns the count (or -error). */
+int sp_stage_draft_profile(sp_stage* s, long long* host, int max);
 
 /* Draft chain: gate = tip.valid && tip.conf >= cutoff; out <- tip. */
 int sp_stage_chain_begin(sp_stage* s, float cutoff, sp_row_result* out,

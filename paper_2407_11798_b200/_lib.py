@@ -25,8 +25,10 @@ SP_ARCH_REF, SP_ARCH_LLAMA = 0, 1
 SP_DTYPE_F32, SP_DTYPE_BF16 = 0, 1
 SP_KIND_PREFILL, SP_KIND_NONSPEC, SP_KIND_SPEC = 0, 1, 2
 SP_STATUS_VALID, SP_STATUS_PLACEHOLDER = 0, 1
-SP_FWD_CHECK_COVERAGE, SP_FWD_SKIPPABLE, SP_FWD_CONTINUE = 1, 2, 4
+SP_FWD_CHECK_COVERAGE, SP_FWD_SKIPPABLE, SP_FWD_CONTINUE, SP_FWD_CHAIN = 1, 2, 4, 8
 SP_EPI_STORE, SP_EPI_RESID, SP_EPI_QKV, SP_EPI_GELU, SP_EPI_SWIGLU = range(5)
+SP_STEP_TIP, SP_STEP_CHAIN = 1, 2
+SP_LAYOUT_NATURAL, SP_LAYOUT_TC_TILED = 0, 1
 
 
 class sp_model_dims(C.Structure):
@@ -35,7 +37,7 @@ class sp_model_dims(C.Structure):
                 ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32),
                 ("ffn_dim", C.c_int32), ("max_context", C.c_int32),
                 ("w_dtype", C.c_int32), ("norm_eps", C.c_float),
-                ("rope_theta", C.c_float)]
+                ("rope_theta", C.c_float), ("w_layout", C.c_int32)]
 
 
 class sp_token(C.Structure):
@@ -59,7 +61,7 @@ class sp_gemv_args(C.Structure):
                 ("head_dim", C.c_int32), ("rope_theta", C.c_float),
                 ("toks", C.c_void_p), ("err", C.c_void_p), ("run_state", C.c_void_p),
                 ("run_state_w", C.c_void_p), ("cancel_word", C.c_void_p),
-                ("run_id", C.c_int32)]
+                ("run_id", C.c_int32), ("cache_row0_dev", C.c_void_p)]
 
 
 class sp_tc_args(C.Structure):
@@ -71,8 +73,9 @@ class sp_tc_args(C.Structure):
                 ("rope_theta", C.c_float), ("toks", C.c_void_p), ("ss_in", C.c_void_p),
                 ("ss_nparts", C.c_int32), ("ss_ld", C.c_int32), ("ss_out", C.c_void_p),
                 ("xb_next", C.c_void_p), ("gain_next", C.c_void_p), ("scratch", C.c_void_p),
-                ("tickets", C.c_void_p), ("ksplit", C.c_int32), ("err", C.c_void_p),
-                ("run_state", C.c_void_p)]
+                ("tickets", C.c_void_p), ("ksplit", C.c_int32), ("max_ctas", C.c_int32),
+                ("err", C.c_void_p),
+                ("run_state", C.c_void_p), ("cache_row0_dev", C.c_void_p)]
 
 
 P = C.c_void_p
@@ -98,9 +101,15 @@ PROTOTYPES = {
     "sp_stage_set_layer": (I, [P, I, P, P, P, P, P, P]),
     "sp_stage_set_head": (I, [P, P, P]),
     "sp_stage_set_cancel_table": (I, [P, P, I]),
+    "sp_stage_set_cta_budget": (I, [P, I]),
     "sp_stage_forward": (I, [P, P, I, I, I, I, P, P, P, P, I, P]),
     "sp_stage_forward_range": (I, [P, P, I, I, I, I, P, P, P, P, I, I, I, P]),
     "sp_stage_lmhead": (I, [P, P, P, I, P, P, P, I, I, F, P]),
+    "sp_stage_step": (I, [P, P, I, I, I, I, P, I, I, F, P, P, P, P]),
+    "sp_stage_io": (I, [P, P, P]),
+    "sp_stage_decode_chain": (I, [P, P, I, I, P, I, F, P, P, P]),
+    "sp_stage_truncate": (I, [P, I]),
+    "sp_stage_draft_profile": (I, [P, P, I]),
     "sp_stage_chain_begin": (I, [P, F, P, P]),
     "sp_stage_chain_state": (I, [P, P, P]),
     "sp_stage_invalidate_tip": (I, [P, P]),

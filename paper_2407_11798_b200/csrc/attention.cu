@@ -22,13 +22,19 @@ plan_kernel(const int32_t* __restrict__ cell_pos,
             const uint32_t* __restrict__ cell_mask, int n_old, int row0,
             const sp_token* __restrict__ toks, int n, int max_context,
             int32_t* __restrict__ vis, int32_t* __restrict__ vis_len,
-            int ld_vis, int check_cov, int* err, const int* run_state) {
+            int ld_vis, int check_cov, int* err, const int* run_state,
+            const RunHdr* hdr) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ int cnt[];  // [max_context + 1]
   // a run skipped by its gate is never checked (engine.py:581-590: the
   // coverage check follows the cancellation test)
   if (run_skipped(run_state)) return;
+  if (hdr != nullptr) {          // per-run scalars from the run header
+    n_old = hdr->row0;
+    row0 = hdr->row0;
+    check_cov = (hdr->flags & SP_FWD_CHECK_COVERAGE) != 0;
+  }
   __shared__ int wsum[PLAN_THREADS / 32];
   const int i = blockIdx.x;
   const int tid = threadIdx.x;
@@ -136,18 +142,21 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
   }
   if (run_skipped(a.run_state)) return;
 
-  const int h = blockIdx.x, i = blockIdx.y, s = blockIdx.z;
+  const int h = blockIdx.x, i = blockIdx.y;
   const int len = a.vis_len[i];
   const int ns = (len + ATT_CH - 1) / ATT_CH;
-  if (s == 0 && threadIdx.x == 0 && ns > a.nsplit) set_error(a.err, SP_DEV_PLAN_OVERFLOW);
-  if (s >= ns) return;
-  const int e0 = s * ATT_CH, e1 = min(len, e0 + ATT_CH);
+  if (blockIdx.z == 0 && threadIdx.x == 0 && ns > a.nsplit) set_error(a.err, SP_DEV_PLAN_OVERFLOW);
   const int kh = h / (a.H / a.KH);
   const int kvd = a.KH * HD;
   const int tid = threadIdx.x, g = tid / LPR, l = tid % LPR;
   const int32_t* plan = a.vis + (size_t)i * a.ld_vis;
   const T* Kc = reinterpret_cast<const T*>(a.k) + kh * HD + l * VEC;
   const T* Vc = reinterpret_cast<const T*>(a.v) + kh * HD + l * VEC;
+  const size_t obase = (size_t)i * a.H * HD + h * HD;
+  auto store = [&](int d, float v) {
+    if (a.out_bf16) reinterpret_cast<__nv_bfloat16*>(a.out)[obase + d] = __float2bfloat16_rn(v);
+    else a.out[obase + d] = v;
+  };
 
   float qv[VEC];
   {
@@ -156,131 +165,135 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
     for (int j = 0; j < VEC; ++j) qv[j] = qp[j] * a.scale;
   }
 
-  // scores
-  for (int eb = e0; eb < e1; eb += G * ATT_UNROLL) {
-    uint4 kv[ATT_UNROLL];
+  // splits s = z, z + gridDim.z, ...: the grid is sized for the machine, not
+  // the context, so one launch shape (and one captured graph) serves any
+  // context length; each split's partial is independent of which CTA ran it
+  for (int s = blockIdx.z; s < ns; s += gridDim.z) {
+    const int e0 = s * ATT_CH, e1 = min(len, e0 + ATT_CH);
+    // scores
+    for (int eb = e0; eb < e1; eb += G * ATT_UNROLL) {
+      uint4 kv[ATT_UNROLL];
 #pragma unroll
-    for (int u = 0; u < ATT_UNROLL; ++u) {
-      const int e = eb + u * G + g;
-      const int row = e < e1 ? plan[e] : plan[e0];
-      kv[u] = ld_stream16(Kc + (size_t)row * kvd);
-    }
+      for (int u = 0; u < ATT_UNROLL; ++u) {
+        const int e = eb + u * G + g;
+        const int row = e < e1 ? plan[e] : plan[e0];
+        kv[u] = ld_stream16(Kc + (size_t)row * kvd);
+      }
 #pragma unroll
-    for (int u = 0; u < ATT_UNROLL; ++u) {
-      float kf[VEC];
-      VecTraits<T>::unpack(kv[u], kf);
-      float d = 0.f;
+      for (int u = 0; u < ATT_UNROLL; ++u) {
+        float kf[VEC];
+        VecTraits<T>::unpack(kv[u], kf);
+        float d = 0.f;
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) d = __fmaf_rn(qv[j], kf[j], d);
+        for (int j = 0; j < VEC; ++j) d = __fmaf_rn(qv[j], kf[j], d);
 #pragma unroll
-      for (int o = LPR / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-      const int e = eb + u * G + g;
-      if (l == 0 && e < e1) sc[e - e0] = d;
-    }
-  }
-  __syncthreads();
-  const int cntv = e1 - e0;
-  float mx = -INFINITY;
-  for (int e = tid; e < cntv; e += ATT_THREADS) mx = fmaxf(mx, sc[e]);
-  mx = warp_max(mx);
-  if ((tid & 31) == 0) red[tid >> 5] = mx;
-  __syncthreads();
-  mx = red[0];
-#pragma unroll
-  for (int w = 1; w < ATT_THREADS / 32; ++w) mx = fmaxf(mx, red[w]);
-  __syncthreads();
-  float sum = 0.f;
-  for (int e = tid; e < cntv; e += ATT_THREADS) {
-    const float p = __expf(sc[e] - mx);
-    sc[e] = p;
-    sum += p;
-  }
-  sum = warp_sum(sum);
-  if ((tid & 31) == 0) red[tid >> 5] = sum;
-  __syncthreads();
-  sum = red[0];
-#pragma unroll
-  for (int w = 1; w < ATT_THREADS / 32; ++w) sum += red[w];
-
-  // P @ V
-  float acc[VEC];
-#pragma unroll
-  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
-  for (int eb = e0; eb < e1; eb += G * ATT_UNROLL) {
-    uint4 vv[ATT_UNROLL];
-#pragma unroll
-    for (int u = 0; u < ATT_UNROLL; ++u) {
-      const int e = eb + u * G + g;
-      const int row = e < e1 ? plan[e] : plan[e0];
-      vv[u] = ld_stream16(Vc + (size_t)row * kvd);
-    }
-#pragma unroll
-    for (int u = 0; u < ATT_UNROLL; ++u) {
-      const int e = eb + u * G + g;
-      if (e < e1) {
-        float vf[VEC];
-        VecTraits<T>::unpack(vv[u], vf);
-        const float p = sc[e - e0];
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) acc[j] = __fmaf_rn(p, vf[j], acc[j]);
+        for (int o = LPR / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        const int e = eb + u * G + g;
+        if (l == 0 && e < e1) sc[e - e0] = d;
       }
     }
-  }
+    __syncthreads();
+    const int cntv = e1 - e0;
+    float mx = -INFINITY;
+    for (int e = tid; e < cntv; e += ATT_THREADS) mx = fmaxf(mx, sc[e]);
+    mx = warp_max(mx);
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
 #pragma unroll
-  for (int j = 0; j < VEC; ++j) part[g][l * VEC + j] = acc[j];
-  __syncthreads();
+    for (int w = 1; w < ATT_THREADS / 32; ++w) mx = fmaxf(mx, red[w]);
+    __syncthreads();
+    float sum = 0.f;
+    for (int e = tid; e < cntv; e += ATT_THREADS) {
+      const float p = __expf(sc[e] - mx);
+      sc[e] = p;
+      sum += p;
+    }
+    sum = warp_sum(sum);
+    if ((tid & 31) == 0) red[tid >> 5] = sum;
+    __syncthreads();
+    sum = red[0];
+#pragma unroll
+    for (int w = 1; w < ATT_THREADS / 32; ++w) sum += red[w];
 
-  const size_t obase = (size_t)i * a.H * HD + h * HD;
-  auto store = [&](int d, float v) {
-    if (a.out_bf16) reinterpret_cast<__nv_bfloat16*>(a.out)[obase + d] = __float2bfloat16_rn(v);
-    else a.out[obase + d] = v;
-  };
-  if (ns == 1) {
+    // P @ V
+    float acc[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
+    for (int eb = e0; eb < e1; eb += G * ATT_UNROLL) {
+      uint4 vv[ATT_UNROLL];
+#pragma unroll
+      for (int u = 0; u < ATT_UNROLL; ++u) {
+        const int e = eb + u * G + g;
+        const int row = e < e1 ? plan[e] : plan[e0];
+        vv[u] = ld_stream16(Vc + (size_t)row * kvd);
+      }
+#pragma unroll
+      for (int u = 0; u < ATT_UNROLL; ++u) {
+        const int e = eb + u * G + g;
+        if (e < e1) {
+          float vf[VEC];
+          VecTraits<T>::unpack(vv[u], vf);
+          const float p = sc[e - e0];
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) acc[j] = __fmaf_rn(p, vf[j], acc[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) part[g][l * VEC + j] = acc[j];
+    __syncthreads();
+
+    if (ns == 1) {
+      for (int d = tid; d < HD; d += ATT_THREADS) {
+        float o = part[0][d];
+        for (int gg = 1; gg < G; ++gg) o += part[gg][d];
+        store(d, o / sum);
+      }
+      return;
+    }
+    float* sp_ = a.scratch + (((size_t)i * a.H + h) * a.nsplit + s) * (HD + 2);
     for (int d = tid; d < HD; d += ATT_THREADS) {
       float o = part[0][d];
       for (int gg = 1; gg < G; ++gg) o += part[gg][d];
-      store(d, o / sum);
+      sp_[2 + d] = o;
     }
-    return;
-  }
-  float* sp_ = a.scratch + (((size_t)i * a.H + h) * a.nsplit + s) * (HD + 2);
-  for (int d = tid; d < HD; d += ATT_THREADS) {
-    float o = part[0][d];
-    for (int gg = 1; gg < G; ++gg) o += part[gg][d];
-    sp_[2 + d] = o;
-  }
-  if (tid == 0) { sp_[0] = mx; sp_[1] = sum; }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const int t = atomicAdd(&a.tickets[i * a.H + h], 1);
-    last = (t == ns - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const float* base = a.scratch + ((size_t)i * a.H + h) * a.nsplit * (HD + 2);
-  float M = -INFINITY;
-  for (int ss = 0; ss < ns; ++ss) M = fmaxf(M, ld_volatile_f(base + ss * (HD + 2)));
-  float L = 0.f;
-  for (int ss = 0; ss < ns; ++ss) {
-    const float* b = base + ss * (HD + 2);
-    L += ld_volatile_f(b + 1) * __expf(ld_volatile_f(b) - M);
-  }
-  for (int d = tid; d < HD; d += ATT_THREADS) {
-    float o = 0.f;
+    if (tid == 0) { sp_[0] = mx; sp_[1] = sum; }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const int t = atomicAdd(&a.tickets[i * a.H + h], 1);
+      last = (t == ns - 1);
+    }
+    __syncthreads();
+    if (!last) continue;  // (sc/part/red are rewritten only after a barrier)
+    __threadfence();
+    const float* base = a.scratch + ((size_t)i * a.H + h) * a.nsplit * (HD + 2);
+    float M = -INFINITY;
+    for (int ss = 0; ss < ns; ++ss) M = fmaxf(M, ld_volatile_f(base + ss * (HD + 2)));
+    float L = 0.f;
     for (int ss = 0; ss < ns; ++ss) {
       const float* b = base + ss * (HD + 2);
-      o += ld_volatile_f(b + 2 + d) * __expf(ld_volatile_f(b) - M);
+      L += ld_volatile_f(b + 1) * __expf(ld_volatile_f(b) - M);
     }
-    store(d, o / L);
+    for (int d = tid; d < HD; d += ATT_THREADS) {
+      float o = 0.f;
+      for (int ss = 0; ss < ns; ++ss) {
+        const float* b = base + ss * (HD + 2);
+        o += ld_volatile_f(b + 2 + d) * __expf(ld_volatile_f(b) - M);
+      }
+      store(d, o / L);
+    }
+    if (tid == 0) a.tickets[i * a.H + h] = 0;
+    return;
   }
-  if (tid == 0) a.tickets[i * a.H + h] = 0;
 }
 
 template <typename T>
 static cudaError_t attn_dispatch(const AttnArgs& a, int hd, cudaStream_t st) {
-  const dim3 grid(a.H, a.n, a.nsplit);
+  // about 4 CTAs per SM in total; splits beyond gridDim.z loop in-CTA
+  const int want = (4 * 148 + a.H * a.n - 1) / (a.H * a.n);
+  const dim3 grid(a.H, a.n, max(1, min(a.nsplit, want)));
   switch (hd) {
     case 8: return launch_pdl(attn_kernel<T, 8>, grid, dim3(ATT_THREADS), 0, st, a);
     case 16: return launch_pdl(attn_kernel<T, 16>, grid, dim3(ATT_THREADS), 0, st, a);
@@ -295,7 +308,7 @@ cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
                         int n_old, int row0, const sp_token* toks, int n,
                         int max_context, int32_t* vis, int32_t* vis_len,
                         int ld_vis, int check_cov, int* err, cudaStream_t st,
-                        const int* run_state) {
+                        const int* run_state, const RunHdr* hdr) {
   const size_t smem = (size_t)(max_context + 1) * sizeof(int);
   static int configured = 0;
   if (smem > 48 * 1024 && configured < (int)smem) {
@@ -305,7 +318,7 @@ cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
   }
   return launch_pdl(plan_kernel, dim3(n), dim3(PLAN_THREADS), smem, st, cell_pos, cell_mask,
                     n_old, row0, toks, n, max_context, vis, vis_len, ld_vis, check_cov, err,
-                    run_state);
+                    run_state, hdr);
 }
 
 cudaError_t launch_attention(const AttnArgs& a, int kv_dtype, int hd,

@@ -77,7 +77,8 @@ gemv_kernel(const sp_gemv_args a) {
             out[(size_t)mi * a.ldo + d1] = o1;
           } else {
             void* cache = (sec == 1) ? a.k_cache : a.v_cache;
-            const size_t base = (size_t)(a.cache_row0 + mi) * a.kv_rows;
+            const int crow = a.cache_row0_dev ? *a.cache_row0_dev : a.cache_row0;
+            const size_t base = (size_t)(crow + mi) * a.kv_rows;
             store_cache<T>(cache, base + d0, o0);
             store_cache<T>(cache, base + d1, o1);
           }

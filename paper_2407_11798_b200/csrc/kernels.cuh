@@ -9,6 +9,21 @@ namespace sp {
 
 typedef sp_tc_args TcArgs;
 
+// Per-run scalars read by the kernels of a stage-run (one small H2D copy per
+// run); followed in memory by int32 rows[max_tokens] and sp_token
+// toks[max_tokens].  Keeping them out of kernel arguments makes a stage-run
+// replayable as a CUDA graph.
+struct RunHdr {
+  int32_t row0;        // first cell row of the run's tokens
+  int32_t n;           // tokens
+  int32_t run_id;
+  int32_t kind;
+  int32_t flags;       // SP_FWD_*
+  int32_t nrows;       // flagged rows for the LM head
+  int32_t cancel_idx;  // run_id % cancel table size, -1 if none
+  float cutoff;        // draft chain: conf >= cutoff keeps the gate open
+};
+
 struct AttnArgs {
   const float* q;
   const void* k;
@@ -49,16 +64,78 @@ struct LmArgs {
   int* err_out;     // optional: copy of *err after the merge
   const int* run_state;
   int* tip;         // device-side draft chain: [argmax, conf bits, valid]
+  int* status_out;  // optional: run status (valid / placeholder)
+  const RunHdr* hdr;  // optional: cutoff from the run header
   int* gate;
   int chain_gate;
   float cutoff;
 };
 
+// ---- K15: persistent draft chain (draft.cu) --------------------------------
+constexpr int DR_NT = 4;          // max fed tokens per launch
+constexpr int DR_MAX_STEPS = 64;  // max chained steps per launch
+constexpr int DR_MAX_LAYERS = 64;
+
+struct DraftLayer {
+  const __nv_bfloat16* qkv;
+  const __nv_bfloat16* o;
+  const __nv_bfloat16* up;
+  const __nv_bfloat16* down;
+  const float* g_attn;
+  const float* g_mlp;
+};
+
+struct DraftHdr {                 // per-launch run header (one H2D copy)
+  int32_t n_feed, steps, pos0, row0, chain, pad0, pad1, pad2;
+  float cutoff;
+  int32_t pad3[3];
+  int32_t tok[DR_NT + DR_MAX_STEPS];   // fed tokens, then explicit step tokens
+};
+
+struct DraftArgs {
+  const DraftLayer* layers;
+  int L, V, d, H, KH, hd, f;
+  float eps, theta;
+  const __nv_bfloat16* emb;
+  const __nv_bfloat16* w_out;
+  const float* g_final;
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
+  size_t kv_layer_elems;
+  int32_t* cell_pos;
+  uint32_t* cell_mask;
+  const DraftHdr* hdr;
+  int* tip;
+  int* gate;
+  float* x;          // [DR_NT, d]
+  float* q;          // [DR_NT, H*hd]
+  float* attn;       // [DR_NT, H*hd]
+  float* h;          // [DR_NT, f]
+  float* att_part;   // [DR_NT, H, max_split, hd + 2]
+  int* att_tick;     // [DR_NT * H]
+  int max_split;
+  LmPartial* lm_part;  // [grid]
+  unsigned* bar;
+  sp_row_result* out;  // [steps + 1]
+  int* err;
+  int* err_out;
+  long long* prof;     // optional: CTA 0's clock64 at every phase edge
+  float* xb;           // [DR_NT, d] x after attention (residual owners' rows)
+  float* opart;        // [DR_NT, H, d] per-head O projections
+  int bufA, bufD, bufE;  // per-CTA weight staging buffers (bytes)
+  int kmax;
+};
+
+size_t draft_smem_bytes(const DraftArgs& a);
+cudaError_t launch_draft_chain(const DraftArgs& a, int ctas, cudaStream_t st);
+int draft_max_ctas(const DraftArgs& a);
+void draft_buffers(DraftArgs& a, int ctas);
+
 cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
                         int n_old, int row0, const sp_token* toks, int n,
                         int max_context, int32_t* vis, int32_t* vis_len,
                         int ld_vis, int check_cov, int* err, cudaStream_t st,
-                        const int* run_state = nullptr);
+                        const int* run_state = nullptr, const RunHdr* hdr = nullptr);
 cudaError_t launch_attention(const AttnArgs& a, int kv_dtype, int hd,
                              cudaStream_t st);
 int attn_splits(int max_len);

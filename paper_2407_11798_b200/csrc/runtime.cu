@@ -11,6 +11,7 @@
 //   epilogue (purge of skipped runs, placeholder status)
 // and never synchronises with the host.  Cell rows are handed out in run
 // order by the host, identically on every stage.
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -50,23 +51,26 @@ __global__ void embed_kernel(const T* __restrict__ emb,
 
 // Stage-run prologue: fold cancel word / upstream placeholder / draft-chain
 // gate into run_state, take token 0 from the chain if asked, write metadata.
-__global__ void gate_kernel(sp_token* toks, int n, int kind, int flags,
-                            const int* cancel_word, int run_id,
-                            const int* in_status, const int* gate,
-                            const int* chain_tip, int* run_state,
-                            int32_t* cell_pos, uint32_t* cell_mask, int row0,
+// Every per-run scalar comes from the device run header, so the same launch
+// (or captured graph) serves every run.
+__global__ void gate_kernel(const RunHdr* hdr, sp_token* toks, const int* cancel_table,
+                            const int* in_status, const int* gate, const int* chain_tip,
+                            int* run_state, int32_t* cell_pos, uint32_t* cell_mask,
                             int n_seq, int max_context, int* err) {
   pdl_wait();
   pdl_trigger();
   __shared__ int skip;
+  const int n = hdr->n, row0 = hdr->row0, flags = hdr->flags;
   if (threadIdx.x == 0) {
     int s = 0;
-    if ((flags & SP_FWD_SKIPPABLE) && kind == SP_KIND_SPEC) {
-      if (cancel_word && ld_volatile(cancel_word) == run_id) s = 1;
+    if ((flags & SP_FWD_SKIPPABLE) && hdr->kind == SP_KIND_SPEC) {
+      if (cancel_table && hdr->cancel_idx >= 0 &&
+          ld_volatile(cancel_table + hdr->cancel_idx) == hdr->run_id)
+        s = 1;
       if (in_status && ld_volatile(in_status) == SP_STATUS_PLACEHOLDER) s = 1;
     }
-    if (gate && ld_volatile(gate) == 0) s = 1;
-    if (chain_tip) toks[0].token = chain_tip[0];
+    if ((flags & SP_FWD_CHAIN) && gate && ld_volatile(gate) == 0) s = 1;
+    if ((flags & SP_FWD_CHAIN) && chain_tip) toks[0].token = chain_tip[0];
     *run_state = s;
     skip = s;
   }
@@ -83,9 +87,9 @@ __global__ void gate_kernel(sp_token* toks, int n, int kind, int flags,
 // Stage-run epilogue: a skipped/abandoned speculative run purges the
 // partitions it wrote under (engine.py:556-561, 581-585, 602-612) and its
 // own cells; the outgoing message is a placeholder (engine.py:545-554).
-__global__ void epilogue_kernel(const sp_token* toks, int n, const int* run_state,
-                                const int32_t* cell_pos, uint32_t* cell_mask,
-                                int n_cells, int row0, int* out_status) {
+__global__ void epilogue_kernel(const RunHdr* hdr, const sp_token* toks,
+                                const int* run_state, const int32_t* cell_pos,
+                                uint32_t* cell_mask, int* out_status) {
   pdl_wait();
   pdl_trigger();
   const int skip = ld_volatile(run_state);
@@ -93,6 +97,7 @@ __global__ void epilogue_kernel(const sp_token* toks, int n, const int* run_stat
     if (out_status && blockIdx.x == 0 && threadIdx.x == 0) *out_status = SP_STATUS_VALID;
     return;
   }
+  const int n = hdr->n, row0 = hdr->row0, n_cells = row0 + n;
   uint32_t purge = 0;
   for (int i = 0; i < n; ++i) purge |= toks[i].seq_mask;
   purge &= ~1u;
@@ -146,10 +151,12 @@ __global__ void prep_kernel(const float* __restrict__ x, int d,
 // folds the device-visible cancel word into run_state; kernels launched
 // after it skip.  A dedicated launch keeps every multi-CTA kernel's view of
 // run_state consistent (no mid-kernel flips).
-__global__ void observe_kernel(const int* cancel_word, int run_id, int* run_state) {
+__global__ void observe_kernel(const RunHdr* hdr, const int* cancel_table, int* run_state) {
   pdl_wait();
   pdl_trigger();
-  if (ld_volatile(cancel_word) == run_id) *run_state = 1;
+  if (!(hdr->flags & SP_FWD_SKIPPABLE) || hdr->kind != SP_KIND_SPEC || hdr->cancel_idx < 0)
+    return;
+  if (ld_volatile(cancel_table + hdr->cancel_idx) == hdr->run_id) *run_state = 1;
 }
 
 __global__ void chain_begin_kernel(const int* tip, int* gate, float cutoff,
@@ -204,6 +211,7 @@ struct sp_stage {
   int cancel_size = 0;
 
   bool tc = false;                       // bf16 llama path on tcgen05
+  int tc_ctas = 0;                       // CTA budget of the GEMMs (0 = all SMs)
   __nv_bfloat16* xb = nullptr;           // [mt, d]   normed input (x * gain)
   __nv_bfloat16* attnb = nullptr;        // [mt, q]   attention output
   __nv_bfloat16* hb = nullptr;           // [mt, ffn] SwiGLU output
@@ -236,19 +244,38 @@ struct sp_stage {
   int* tip = nullptr;   // [argmax, conf bits, valid]
   int* gate = nullptr;
 
-  sp_token* desc_dev = nullptr;
-  sp_token* desc_host = nullptr;
-  int32_t* rows_dev = nullptr;
-  int32_t* rows_host = nullptr;
+  // run header (device) + its pinned host staging ring
+  RunHdr* hdr = nullptr;
+  int32_t* hdr_rows = nullptr;           // inside hdr
+  sp_token* hdr_toks = nullptr;          // inside hdr
+  size_t hdr_bytes = 0;
+  uint8_t* hdr_host = nullptr;           // [DESC_RING][hdr_bytes]
   cudaEvent_t ev[DESC_RING];
   int slot = 0;
 
-  // last forward (for lmhead row gathering and the epilogue)
-  const sp_token* cur_desc = nullptr;
+  // fixed outputs of graph-replayed steps
+  float* gx_out = nullptr;               // [max_tokens * d + 4] (x then status)
+  sp_row_result* gres = nullptr;         // [1 + max_tokens]: header row + rows
+  std::map<std::vector<long>, cudaGraphExec_t> graphs;
+  std::map<std::vector<long>, int> seen;
+  bool use_graphs = true;
+
+  // K15 draft chain (persistent kernel)
+  DraftLayer* dlayers = nullptr;         // device copy of the layer table
+  bool dlayers_dirty = true;
+  DraftHdr* dhdr = nullptr;
+  unsigned* dbar = nullptr;
+  int draft_ctas = 0;
+  long long* dprof = nullptr;            // SP_DRAFT_PROF: phase timestamps
+  float* dxb = nullptr;
+  float* dopart = nullptr;
+
+  // last forward (split evaluation continues it)
   int cur_n = 0;
   int cur_row0 = 0;
   int cur_max_pos = 0;
   int cur_flags = 0;
+  bool cur_valid = false;
 };
 
 static int cuda_status(cudaError_t e) { return e == cudaSuccess ? SP_OK : SP_ERR_CUDA; }
@@ -312,7 +339,12 @@ extern "C" int sp_stage_create(const sp_model_dims* dims, int layer_lo,
   alloc((void**)&s->tip, sizeof(int) * 4);
   alloc((void**)&s->gate, sizeof(int));
   // bf16 (llama) stages run on the tensor-core path with tiled weights
-  s->tc = d.arch == SP_ARCH_LLAMA && d.w_dtype == SP_DTYPE_BF16;
+  s->tc = d.arch == SP_ARCH_LLAMA && d.w_dtype == SP_DTYPE_BF16 &&
+          d.w_layout == SP_LAYOUT_TC_TILED;
+  if (d.w_layout == SP_LAYOUT_TC_TILED && !s->tc) {
+    delete s;
+    return SP_ERR_ARG;
+  }
   if (s->tc && (d.d_model % 128 || s->q_dim % 128 || (s->q_dim + 2 * s->kv_dim) % 128 ||
                 d.ffn_dim % 64)) {
     delete s;
@@ -335,10 +367,16 @@ extern "C" int sp_stage_create(const sp_model_dims* dims, int layer_lo,
       }
     }
   }
-  alloc((void**)&s->desc_dev, sizeof(sp_token) * (size_t)mt * DESC_RING);
-  alloc((void**)&s->rows_dev, sizeof(int32_t) * (size_t)mt * DESC_RING);
-  if (ok && cudaMallocHost((void**)&s->desc_host, sizeof(sp_token) * (size_t)mt * DESC_RING) != cudaSuccess) ok = false;
-  if (ok && cudaMallocHost((void**)&s->rows_host, sizeof(int32_t) * (size_t)mt * DESC_RING) != cudaSuccess) ok = false;
+  s->hdr_bytes = sizeof(RunHdr) + sizeof(int32_t) * (size_t)mt + sizeof(sp_token) * (size_t)mt;
+  alloc((void**)&s->hdr, s->hdr_bytes);
+  if (ok) {
+    s->hdr_rows = reinterpret_cast<int32_t*>(s->hdr + 1);
+    s->hdr_toks = reinterpret_cast<sp_token*>(s->hdr_rows + mt);
+  }
+  if (ok && cudaMallocHost((void**)&s->hdr_host, s->hdr_bytes * DESC_RING) != cudaSuccess) ok = false;
+  alloc((void**)&s->gx_out, sizeof(float) * ((size_t)mt * d.d_model + 4));
+  alloc((void**)&s->gres, sizeof(sp_row_result) * (size_t)(mt + 1));
+  s->use_graphs = getenv("SP_NO_GRAPHS") == nullptr;
   for (int i = 0; ok && i < DESC_RING; ++i)
     if (cudaEventCreateWithFlags(&s->ev[i], cudaEventDisableTiming) != cudaSuccess) ok = false;
   if (ok) ok = cudaDeviceSynchronize() == cudaSuccess;
@@ -356,11 +394,12 @@ extern "C" int sp_stage_destroy(sp_stage* s) {
   void* ptrs[] = {s->cell_pos, s->cell_mask, s->kc, s->vc, s->q, s->attn, s->h,
                   s->xg, s->vis, s->vis_len, s->att_scratch, s->att_tickets,
                   s->lm_scratch, s->lm_ticket, s->err, s->run_state, s->tip,
-                  s->gate, s->desc_dev, s->rows_dev, s->xb, s->attnb, s->hb, s->ss,
-                  s->tc_scratch, s->tc_tickets};
+                  s->gate, s->hdr, s->xb, s->attnb, s->hb, s->ss,
+                  s->tc_scratch, s->tc_tickets, s->gx_out, s->gres,
+                  s->dlayers, s->dhdr, s->dbar, s->dprof, s->dxb, s->dopart};
+  for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
   for (void* p : ptrs) if (p) cudaFree(p);
-  if (s->desc_host) cudaFreeHost(s->desc_host);
-  if (s->rows_host) cudaFreeHost(s->rows_host);
+  if (s->hdr_host) cudaFreeHost(s->hdr_host);
   for (int i = 0; i < DESC_RING; ++i) if (s->ev[i]) cudaEventDestroy(s->ev[i]);
   delete s;
   return SP_OK;
@@ -382,6 +421,7 @@ extern "C" int sp_stage_set_layer(sp_stage* s, int layer, const void* w_qkv,
   LayerW& L = s->layers[layer - s->lo];
   L.qkv = w_qkv; L.o = w_o; L.up = w_up; L.down = w_down;
   L.attn_norm = attn_norm; L.mlp_norm = mlp_norm;
+  s->dlayers_dirty = true;
   return SP_OK;
 }
 
@@ -393,8 +433,22 @@ extern "C" int sp_stage_set_head(sp_stage* s, const void* w_out,
   return SP_OK;
 }
 
+static void drop_graphs(sp_stage* s) {
+  for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
+  s->graphs.clear();
+  s->seen.clear();
+}
+
+extern "C" int sp_stage_set_cta_budget(sp_stage* s, int ctas) {
+  if (!s || ctas < 0) return SP_ERR_ARG;
+  s->tc_ctas = ctas;
+  drop_graphs(s);
+  return SP_OK;
+}
+
 extern "C" int sp_stage_set_cancel_table(sp_stage* s, const int* table, int size) {
   if (!s || (table && size <= 0)) return SP_ERR_ARG;
+  drop_graphs(s);
   s->cancel_table = table;
   s->cancel_size = size;
   return SP_OK;
@@ -407,90 +461,98 @@ static int next_slot(sp_stage* s) {
   return k;
 }
 
-extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
-                                      int n, int run_id, int kind, int flags,
-                                      const float* x_in, const int* in_status,
-                                      float* x_out, int* out_status, int chain,
-                                      int layer_a, int layer_b, void* stream) {
-  if (!s || n <= 0 || !x_out) return SP_ERR_ARG;
-  if (layer_a < 0) { layer_a = s->lo; layer_b = s->hi; }
-  if (layer_a < s->lo || layer_b > s->hi || layer_b <= layer_a) return SP_ERR_MODEL;
-  const bool cont = (flags & SP_FWD_CONTINUE) != 0;
-  if (n > s->max_tokens) return SP_ERR_CAPACITY;
-  if (!cont && (!host_toks || s->n_cells + n > s->cap)) return SP_ERR_CAPACITY;
-  if (cont && (s->cur_desc == nullptr || s->cur_n != n)) return SP_ERR_PROTOCOL;
-  if (layer_a == 0 && !s->emb) return SP_ERR_ARG;
-  if (layer_a > 0 && !x_in) return SP_ERR_MODEL;  // model.py:361-362
-  for (int l = layer_a; l < layer_b; ++l)
-    if (!s->layers[l - s->lo].qkv) return SP_ERR_ARG;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+// RUN_CONFIG (engine.py:231-251): per-run scalars + descriptor -> the device
+// run header, one stream-ordered H2D copy from a pinned ring slot.
+static cudaError_t write_hdr(sp_stage* s, const sp_token* toks, int n, int run_id, int kind,
+                             int flags, const int32_t* rows, int nrows, float cutoff,
+                             cudaStream_t st) {
+  const int k = next_slot(s);
+  uint8_t* h = s->hdr_host + (size_t)k * s->hdr_bytes;
+  RunHdr* rh = reinterpret_cast<RunHdr*>(h);
+  int32_t* hr = reinterpret_cast<int32_t*>(rh + 1);
+  sp_token* ht = reinterpret_cast<sp_token*>(hr + s->max_tokens);
+  rh->row0 = s->n_cells;
+  rh->n = n;
+  rh->run_id = run_id;
+  rh->kind = kind;
+  rh->flags = flags;
+  rh->nrows = nrows;
+  rh->cancel_idx = (s->cancel_table && (flags & SP_FWD_SKIPPABLE) && kind == SP_KIND_SPEC)
+                       ? run_id % s->cancel_size : -1;
+  rh->cutoff = cutoff;
+  for (int i = 0; i < nrows; ++i) hr[i] = rows[i];
+  for (int i = 0; i < n; ++i) ht[i] = toks[i];
+  const size_t bytes = (const uint8_t*)(ht + n) - h;
+  cudaError_t e = cudaMemcpyAsync(s->hdr, h, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaEventRecord(s->ev[k], st);
+  return e;
+}
+
+struct RunIO {
+  const float* x_in;       // stage input activations (NULL on layer 0)
+  const int* in_status;
+  float* x_out;
+  int* out_status;
+};
+
+struct HeadIO {            // fused LM head over the header's rows
+  int nrows = 0;
+  sp_row_result* out = nullptr;
+  int* err_out = nullptr;
+  int* status_out = nullptr;
+  float* logits = nullptr;
+  int update_tip = 0;
+  int chain_gate = 0;
+};
+
+// Enqueue one stage-run (layers [layer_a, layer_b)) reading every per-run
+// scalar from the device header.  ``graphable``: no host-dependent launch
+// shapes (the attention bound is the context cap) so the sequence can be
+// captured once and replayed for any run of the same token count.
+static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
+                       int max_pos, bool coverage, bool graphable, const RunIO& io,
+                       const HeadIO* head, cudaStream_t st) {
   const sp_model_dims& D = s->dims;
   const int d = D.d_model;
-
-  sp_token* dd;
-  int row0, n_old, max_pos;
+  void* stream = reinterpret_cast<void*>(st);
   if (!cont) {
-    // RUN_CONFIG: stream-ordered descriptor (engine.py:231-251)
-    const int k = next_slot(s);
-    sp_token* hd = s->desc_host + (size_t)k * s->max_tokens;
-    dd = s->desc_dev + (size_t)k * s->max_tokens;
-    max_pos = 0;
-    for (int i = 0; i < n; ++i) {
-      hd[i] = host_toks[i];
-      max_pos = host_toks[i].pos > max_pos ? host_toks[i].pos : max_pos;
-    }
-    SP_CHECK(cudaMemcpyAsync(dd, hd, sizeof(sp_token) * n, cudaMemcpyHostToDevice, st));
-    SP_CHECK(cudaEventRecord(s->ev[k], st));
-    row0 = s->n_cells;
-    n_old = s->n_cells;
-    s->n_cells += n;
-    s->cur_desc = dd; s->cur_n = n; s->cur_row0 = row0; s->cur_max_pos = max_pos;
-    s->cur_flags = flags;
-  } else {
-    dd = const_cast<sp_token*>(s->cur_desc);
-    row0 = s->cur_row0;
-    n_old = row0;
-    max_pos = s->cur_max_pos;
-    flags = s->cur_flags | SP_FWD_CONTINUE;
+    SP_CHECK(launch_pdl(gate_kernel, dim3(1), dim3(128), 0, st, (const RunHdr*)s->hdr,
+                        s->hdr_toks, s->cancel_table, io.in_status,
+                        (const int*)s->gate, (const int*)s->tip, s->run_state, s->cell_pos,
+                        s->cell_mask, s->n_seq, D.max_context, s->err));
   }
-  const int* cancel_word = (s->cancel_table && (flags & SP_FWD_SKIPPABLE) &&
-                            kind == SP_KIND_SPEC)
-                               ? s->cancel_table + (run_id % s->cancel_size)
-                               : nullptr;
-  if (!cont) {
-    SP_CHECK(launch_pdl(gate_kernel, dim3(1), dim3(128), 0, st, dd, n, kind, flags,
-                        cancel_word, run_id, in_status, chain ? (const int*)s->gate : nullptr,
-                        chain ? (const int*)s->tip : nullptr, s->run_state, s->cell_pos,
-                        s->cell_mask, row0, s->n_seq, D.max_context, s->err));
-  }
-
   if (layer_a == 0) {
     const int threads = d >= 256 ? 256 : 64;
     if (D.w_dtype == SP_DTYPE_BF16)
       SP_CHECK(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(n), dim3(threads), 0, st,
-                          (const __nv_bfloat16*)s->emb, s->pos_table, (const sp_token*)dd, n, d,
-                          D.vocab, D.max_context, x_out, s->err, (const int*)s->run_state));
+                          (const __nv_bfloat16*)s->emb, s->pos_table,
+                          (const sp_token*)s->hdr_toks, n, d, D.vocab, D.max_context,
+                          io.x_out, s->err, (const int*)s->run_state));
     else
       SP_CHECK(launch_pdl(embed_kernel<float>, dim3(n), dim3(threads), 0, st,
-                          (const float*)s->emb, s->pos_table, (const sp_token*)dd, n, d,
-                          D.vocab, D.max_context, x_out, s->err, (const int*)s->run_state));
-  } else if (x_in != x_out) {
-    SP_CHECK(cudaMemcpyAsync(x_out, x_in, sizeof(float) * (size_t)n * d,
+                          (const float*)s->emb, s->pos_table, (const sp_token*)s->hdr_toks,
+                          n, d, D.vocab, D.max_context, io.x_out, s->err,
+                          (const int*)s->run_state));
+  } else if (io.x_in != io.x_out) {
+    SP_CHECK(cudaMemcpyAsync(io.x_out, io.x_in, sizeof(float) * (size_t)n * d,
                              cudaMemcpyDeviceToDevice, st));
   }
-
-  const int check = (flags & SP_FWD_CHECK_COVERAGE) ? 1 : 0;
   if (!cont)
-    SP_CHECK(launch_plan(s->cell_pos, s->cell_mask, n_old, row0, dd, n,
-                         D.max_context, s->vis, s->vis_len, s->ld_vis, check,
-                         s->err, st, s->run_state));
+    SP_CHECK(launch_plan(s->cell_pos, s->cell_mask, 0, 0, s->hdr_toks, n, D.max_context,
+                         s->vis, s->vis_len, s->ld_vis, 0, s->err, st, s->run_state,
+                         s->hdr));
   // launch bound on visible entries per query (+ self): chain batches see
-  // exactly pos cells; otherwise bounded by the table size
-  const int bound = check ? (max_pos + 1) : (n_old + n);
+  // exactly pos cells; a graph must hold for any run (context cap)
+  const int bound = graphable ? (D.max_context + s->max_tokens)
+                              : (coverage ? (max_pos + 1) : (s->n_cells));
   const int nsplit = attn_splits(bound);
   const size_t need = (size_t)n * D.n_heads * nsplit * (D.head_dim + 2);
   if (need > s->att_scratch_floats) {
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return SP_ERR_CAPACITY;  // the eager first occurrence sizes it
     cudaStreamSynchronize(st);
+    drop_graphs(s);  // captured graphs hold the old scratch pointer
     cudaFree(s->att_scratch);
     if (cudaMalloc((void**)&s->att_scratch, sizeof(float) * need) != cudaSuccess)
       return SP_ERR_CUDA;
@@ -499,6 +561,8 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
 
   const bool llama = D.arch == SP_ARCH_LLAMA;
   const size_t wb = wbytes(D);
+  float* x_out = io.x_out;
+  const int32_t* row0_dev = &s->hdr->row0;
   if (s->tc) {
     // bf16 normed input of layer_a's attention norm + its statistic
     SP_CHECK(launch_pdl(prep_kernel, dim3(n), dim3(256), 0, st, (const float*)x_out, d,
@@ -516,18 +580,19 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
     a.nsplit = nsplit; a.scale = 1.0f / sqrtf((float)D.head_dim);
     a.out = s->attn; a.scratch = s->att_scratch; a.tickets = s->att_tickets;
     a.run_state = s->run_state; a.run_state_w = nullptr;
-    a.cancel_word = nullptr; a.run_id = run_id; a.err = s->err;
+    a.cancel_word = nullptr; a.run_id = 0; a.err = s->err;
     if (s->tc) {
       // ---- tensor-core path (tcgen05, bf16 activations, fp32 accumulate) ----
       TcArgs t{};
-      t.m = n; t.toks = dd; t.err = s->err; t.run_state = s->run_state;
+      t.m = n; t.toks = s->hdr_toks; t.err = s->err; t.run_state = s->run_state;
       t.scratch = s->tc_scratch; t.tickets = s->tc_tickets; t.norm_eps = D.norm_eps;
+      t.max_ctas = s->tc_ctas;
       t.ss_ld = s->max_tokens;
       // q, k, v (+RoPE, K/V into the cell rows): model.py:387-393
       t.n_rows = s->q_dim + 2 * s->kv_dim; t.k = d; t.epi = SP_EPI_QKV; t.norm = 1;
       t.ss_in = s->ss; t.ss_nparts = ss_parts; t.out = s->q; t.ldo = s->q_dim;
       t.q_rows = s->q_dim; t.kv_rows = s->kv_dim; t.k_cache = kl; t.v_cache = vl;
-      t.cache_row0 = row0; t.head_dim = D.head_dim; t.rope_theta = D.rope_theta;
+      t.cache_row0_dev = row0_dev; t.head_dim = D.head_dim; t.rope_theta = D.rope_theta;
       t.w = L.qkv;
       SP_CHECK(launch_tc_gemm(s->m_xb, t, st));
       a.out = reinterpret_cast<float*>(s->attnb); a.out_bf16 = 1;
@@ -558,7 +623,7 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
       g.w_dtype = D.w_dtype;
       g.run_state = s->run_state;
       g.err = s->err;
-      g.toks = dd;
+      g.toks = s->hdr_toks;
       g.m = n;
       // q, k, v (model.py:387-393): rmsnorm fused, k/v into cell rows
       g.w = L.qkv; g.n_rows = s->q_dim + 2 * s->kv_dim; g.k = d;
@@ -566,7 +631,7 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
       g.gain = llama ? L.attn_norm : nullptr;
       g.epi = SP_EPI_QKV; g.out = s->q; g.ldo = s->q_dim;
       g.q_rows = s->q_dim; g.kv_rows = s->kv_dim; g.k_cache = kl; g.v_cache = vl;
-      g.cache_row0 = row0; g.rope = llama ? 1 : 0; g.head_dim = D.head_dim;
+      g.cache_row0_dev = row0_dev; g.rope = llama ? 1 : 0; g.head_dim = D.head_dim;
       g.rope_theta = D.rope_theta;
       int rc = sp_gemv(&g, stream);
       if (rc) return rc;
@@ -574,7 +639,7 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
       SP_CHECK(launch_attention(a, D.w_dtype, D.head_dim, st));
       // x += attn @ Wo (model.py:416)
       g = sp_gemv_args{};
-      g.w_dtype = D.w_dtype; g.run_state = s->run_state; g.err = s->err; g.toks = dd;
+      g.w_dtype = D.w_dtype; g.run_state = s->run_state; g.err = s->err; g.toks = s->hdr_toks;
       g.m = n; g.w = L.o; g.n_rows = d; g.k = s->q_dim; g.x = s->attn; g.ldx = s->q_dim;
       g.norm = 0; g.epi = SP_EPI_RESID; g.out = x_out; g.ldo = d;
       rc = sp_gemv(&g, stream);
@@ -592,16 +657,76 @@ extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
       if (rc) return rc;
     }
     // early inference cancellation: observe the cancel word between layers
-    // (engine.py:602-612 drains cancels between layers)
-    if (cancel_word && l + 1 < layer_b && ((l + 1 - layer_a) % OBSERVE_EVERY) == 0) {
-      SP_CHECK(launch_pdl(observe_kernel, dim3(1), dim3(1), 0, st, cancel_word, run_id,
-                          s->run_state));
-    }
+    // (engine.py:602-612 drains cancels between layers); a no-op for runs
+    // that are not cancellable (read from the header)
+    if (s->cancel_table && l + 1 < layer_b && ((l + 1 - layer_a) % OBSERVE_EVERY) == 0)
+      SP_CHECK(launch_pdl(observe_kernel, dim3(1), dim3(1), 0, st, (const RunHdr*)s->hdr,
+                          s->cancel_table, s->run_state));
   }
-  SP_CHECK(launch_pdl(epilogue_kernel, dim3(max(1, min(148, (s->n_cells + 255) / 256))),
-                      dim3(256), 0, st, (const sp_token*)dd, n, (const int*)s->run_state,
-                      (const int32_t*)s->cell_pos, s->cell_mask, s->n_cells, row0, out_status));
+  SP_CHECK(launch_pdl(epilogue_kernel, dim3(max(1, min(148, (s->cap + 255) / 256))),
+                      dim3(256), 0, st, (const RunHdr*)s->hdr, (const sp_token*)s->hdr_toks,
+                      (const int*)s->run_state, (const int32_t*)s->cell_pos, s->cell_mask,
+                      io.out_status));
+  if (head && head->nrows > 0) {
+    SP_CHECK(launch_pdl(gather_rows_kernel, dim3(head->nrows), dim3(128), 0, st,
+                        (const float*)x_out, d, (const int32_t*)s->hdr_rows, s->xg,
+                        (const int*)s->run_state));
+    LmArgs m{};
+    m.w = s->w_out; m.V = D.vocab; m.d = d; m.x = s->xg; m.n_rows = head->nrows;
+    m.norm = 1; m.eps = D.norm_eps;
+    m.gain = D.arch == SP_ARCH_LLAMA ? s->final_norm : nullptr;
+    m.out = head->out; m.logits = head->logits; m.scratch = s->lm_scratch;
+    m.ticket = s->lm_ticket; m.err = s->err; m.err_out = head->err_out;
+    m.status_out = head->status_out; m.run_state = s->run_state;
+    m.tip = head->update_tip ? s->tip : nullptr;
+    m.gate = head->update_tip ? s->gate : nullptr;
+    m.chain_gate = head->chain_gate;
+    m.hdr = s->hdr;
+    SP_CHECK(launch_lmhead(m, D.w_dtype, st));
+  }
   return SP_OK;
+}
+
+static int check_run(sp_stage* s, const sp_token* toks, int n, int layer_a, int layer_b,
+                     const float* x_in) {
+  if (!s || n <= 0) return SP_ERR_ARG;
+  if (layer_a < s->lo || layer_b > s->hi || layer_b <= layer_a) return SP_ERR_MODEL;
+  if (n > s->max_tokens) return SP_ERR_CAPACITY;
+  if (layer_a == 0 && !s->emb) return SP_ERR_ARG;
+  if (layer_a > 0 && !x_in) return SP_ERR_MODEL;  // model.py:361-362
+  for (int l = layer_a; l < layer_b; ++l)
+    if (!s->layers[l - s->lo].qkv) return SP_ERR_ARG;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_forward_range(sp_stage* s, const sp_token* host_toks,
+                                      int n, int run_id, int kind, int flags,
+                                      const float* x_in, const int* in_status,
+                                      float* x_out, int* out_status, int chain,
+                                      int layer_a, int layer_b, void* stream) {
+  if (!s || !x_out) return SP_ERR_ARG;
+  if (layer_a < 0) { layer_a = s->lo; layer_b = s->hi; }
+  int rc = check_run(s, host_toks, n, layer_a, layer_b, x_in);
+  if (rc) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool cont = (flags & SP_FWD_CONTINUE) != 0;
+  if (cont && (!s->cur_valid || s->cur_n != n)) return SP_ERR_PROTOCOL;
+  if (chain) flags |= SP_FWD_CHAIN;
+  int max_pos = 0;
+  if (!cont) {
+    if (!host_toks || s->n_cells + n > s->cap) return SP_ERR_CAPACITY;
+    for (int i = 0; i < n; ++i) max_pos = host_toks[i].pos > max_pos ? host_toks[i].pos : max_pos;
+    SP_CHECK(write_hdr(s, host_toks, n, run_id, kind, flags & ~SP_FWD_CONTINUE, nullptr, 0,
+                       0.f, st));
+    s->cur_n = n; s->cur_row0 = s->n_cells; s->cur_max_pos = max_pos;
+    s->cur_flags = flags & ~SP_FWD_CONTINUE; s->cur_valid = true;
+    s->n_cells += n;
+  } else {
+    max_pos = s->cur_max_pos;
+  }
+  const bool cov = ((cont ? s->cur_flags : flags) & SP_FWD_CHECK_COVERAGE) != 0;
+  RunIO io{x_in, in_status, x_out, out_status};
+  return enqueue_run(s, n, layer_a, layer_b, cont, max_pos, cov, false, io, nullptr, st);
 }
 
 extern "C" int sp_stage_forward(sp_stage* s, const sp_token* host_toks, int n,
@@ -624,14 +749,18 @@ extern "C" int sp_stage_lmhead(sp_stage* s, const float* x,
   if (n_rows > s->max_tokens) return SP_ERR_CAPACITY;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const sp_model_dims& D = s->dims;
+  // rows + cutoff into the header (the forward's scalars stay as written)
   const int k = next_slot(s);
-  int32_t* hr = s->rows_host + (size_t)k * s->max_tokens;
-  int32_t* dr = s->rows_dev + (size_t)k * s->max_tokens;
+  uint8_t* h = s->hdr_host + (size_t)k * s->hdr_bytes;
+  int32_t* hr = reinterpret_cast<int32_t*>(h);
   for (int i = 0; i < n_rows; ++i) hr[i] = host_rows[i];
-  SP_CHECK(cudaMemcpyAsync(dr, hr, sizeof(int32_t) * n_rows, cudaMemcpyHostToDevice, st));
+  float* hc = reinterpret_cast<float*>(hr + s->max_tokens);
+  *hc = cutoff;
+  SP_CHECK(cudaMemcpyAsync(s->hdr_rows, hr, sizeof(int32_t) * n_rows, cudaMemcpyHostToDevice, st));
+  SP_CHECK(cudaMemcpyAsync(&s->hdr->cutoff, hc, sizeof(float), cudaMemcpyHostToDevice, st));
   SP_CHECK(cudaEventRecord(s->ev[k], st));
   SP_CHECK(launch_pdl(gather_rows_kernel, dim3(n_rows), dim3(128), 0, st, x, D.d_model,
-                      (const int32_t*)dr, s->xg, (const int*)s->run_state));
+                      (const int32_t*)s->hdr_rows, s->xg, (const int*)s->run_state));
   LmArgs a{};
   a.w = s->w_out; a.V = D.vocab; a.d = D.d_model; a.x = s->xg; a.n_rows = n_rows;
   a.norm = 1; a.eps = D.norm_eps;
@@ -642,8 +771,78 @@ extern "C" int sp_stage_lmhead(sp_stage* s, const float* x,
   a.tip = update_tip ? s->tip : nullptr;
   a.gate = update_tip ? s->gate : nullptr;
   a.chain_gate = chain_gate;
-  a.cutoff = cutoff;
+  a.hdr = s->hdr;
   SP_CHECK(launch_lmhead(a, D.w_dtype, st));
+  return SP_OK;
+}
+
+// One decode/verification stage-run (+ fused LM head) replayed from a
+// cached CUDA graph: the run's scalars travel in the header copy, the graph
+// reads x_in/in_status (pointers fixed per key) and writes the stage's fixed
+// buffers (sp_stage_io).  The first occurrence of a shape runs eagerly, the
+// second is captured.
+extern "C" int sp_stage_step(sp_stage* s, const sp_token* host_toks, int n, int run_id,
+                             int kind, int flags, const int32_t* host_rows, int n_rows,
+                             int head_flags, float cutoff, const float* x_in,
+                             const int* in_status, void* res_copy, void* stream) {
+  int rc = check_run(s, host_toks, n, s ? s->lo : 0, s ? s->hi : 0, x_in);
+  if (rc) return rc;
+  if (!host_toks || s->n_cells + n > s->cap) return SP_ERR_CAPACITY;
+  if (n_rows > 0 && (s->hi != s->dims.n_layers || !s->w_out || !host_rows)) return SP_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int d = s->dims.d_model;
+  if (head_flags & SP_STEP_CHAIN) flags |= SP_FWD_CHAIN;
+  SP_CHECK(write_hdr(s, host_toks, n, run_id, kind, flags & ~SP_FWD_CONTINUE, host_rows,
+                     n_rows, cutoff, st));
+  s->cur_valid = false;
+  int max_pos = 0;
+  for (int i = 0; i < n; ++i) max_pos = host_toks[i].pos > max_pos ? host_toks[i].pos : max_pos;
+  s->n_cells += n;
+  RunIO io{x_in, in_status, s->gx_out, reinterpret_cast<int*>(s->gx_out + (size_t)n * d)};
+  HeadIO head;
+  head.nrows = n_rows;
+  head.out = s->gres + 1;
+  head.err_out = &reinterpret_cast<int*>(s->gres)[1];
+  head.status_out = &reinterpret_cast<int*>(s->gres)[0];
+  head.update_tip = (head_flags & (SP_STEP_TIP | SP_STEP_CHAIN)) ? 1 : 0;
+  head.chain_gate = (head_flags & SP_STEP_CHAIN) ? 1 : 0;
+  const bool graphable = s->use_graphs && n <= 16;
+  if (!graphable) {
+    rc = enqueue_run(s, n, s->lo, s->hi, false, max_pos,
+                     (flags & SP_FWD_CHECK_COVERAGE) != 0, false, io, &head, st);
+  } else {
+    const std::vector<long> key = {n, n_rows, head.update_tip, head.chain_gate,
+                                   (long)(uintptr_t)x_in, (long)(uintptr_t)in_status};
+    auto it = s->graphs.find(key);
+    if (it != s->graphs.end()) {
+      SP_CHECK(cudaGraphLaunch(it->second, st));
+    } else if (s->seen[key]++ == 0) {
+      rc = enqueue_run(s, n, s->lo, s->hi, false, max_pos, true, true, io, &head, st);
+    } else {
+      cudaGraph_t g;
+      SP_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      rc = enqueue_run(s, n, s->lo, s->hi, false, max_pos, true, true, io, &head, st);
+      cudaError_t e = cudaStreamEndCapture(st, &g);
+      if (rc) return rc;
+      SP_CHECK(e);
+      cudaGraphExec_t ex;
+      SP_CHECK(cudaGraphInstantiate(&ex, g, 0));
+      cudaGraphDestroy(g);
+      s->graphs[key] = ex;
+      SP_CHECK(cudaGraphLaunch(ex, st));
+    }
+  }
+  if (rc) return rc;
+  if (res_copy && n_rows > 0)
+    SP_CHECK(cudaMemcpyAsync(res_copy, s->gres, sizeof(sp_row_result) * (1 + n_rows),
+                             cudaMemcpyDefault, st));
+  return SP_OK;
+}
+
+extern "C" int sp_stage_io(sp_stage* s, float** x_out, sp_row_result** res) {
+  if (!s) return SP_ERR_ARG;
+  if (x_out) *x_out = s->gx_out;
+  if (res) *res = s->gres;
   return SP_OK;
 }
 
@@ -697,13 +896,9 @@ extern "C" int sp_stage_cache_insert_meta(sp_stage* s, const sp_token* host_toks
   if (!s || !host_toks || n <= 0) return SP_ERR_ARG;
   if (n > s->max_tokens || s->n_cells + n > s->cap) return SP_ERR_CAPACITY;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int k = next_slot(s);
-  sp_token* hd = s->desc_host + (size_t)k * s->max_tokens;
-  sp_token* dd = s->desc_dev + (size_t)k * s->max_tokens;
-  for (int i = 0; i < n; ++i) hd[i] = host_toks[i];
-  SP_CHECK(cudaMemcpyAsync(dd, hd, sizeof(sp_token) * n, cudaMemcpyHostToDevice, st));
-  SP_CHECK(cudaEventRecord(s->ev[k], st));
-  SP_CHECK(launch_meta_write(s->cell_pos, s->cell_mask, s->n_cells, dd, n,
+  SP_CHECK(write_hdr(s, host_toks, n, 0, SP_KIND_PREFILL, 0, nullptr, 0, 0.f, st));
+  s->cur_valid = false;
+  SP_CHECK(launch_meta_write(s->cell_pos, s->cell_mask, s->n_cells, s->hdr_toks, n,
                              s->n_seq, s->dims.max_context, s->err, st));
   s->n_cells += n;
   return SP_OK;
@@ -717,13 +912,9 @@ extern "C" int sp_stage_plan_only(sp_stage* s, const sp_token* host_toks, int n,
   if (!s || !host_toks || n <= 0) return SP_ERR_ARG;
   if (n > s->max_tokens || s->n_cells + n > s->cap) return SP_ERR_CAPACITY;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int k = next_slot(s);
-  sp_token* hd = s->desc_host + (size_t)k * s->max_tokens;
-  sp_token* dd = s->desc_dev + (size_t)k * s->max_tokens;
-  for (int i = 0; i < n; ++i) hd[i] = host_toks[i];
-  SP_CHECK(cudaMemcpyAsync(dd, hd, sizeof(sp_token) * n, cudaMemcpyHostToDevice, st));
-  SP_CHECK(cudaEventRecord(s->ev[k], st));
-  SP_CHECK(launch_plan(s->cell_pos, s->cell_mask, s->n_cells, s->n_cells, dd, n,
+  SP_CHECK(write_hdr(s, host_toks, n, 0, SP_KIND_PREFILL, 0, nullptr, 0, 0.f, st));
+  s->cur_valid = false;
+  SP_CHECK(launch_plan(s->cell_pos, s->cell_mask, s->n_cells, s->n_cells, s->hdr_toks, n,
                        s->dims.max_context, s->vis, s->vis_len, s->ld_vis,
                        check_coverage, s->err, st));
   return SP_OK;
@@ -735,6 +926,7 @@ extern "C" int sp_stage_reset(sp_stage* s, void* stream) {
   SP_CHECK(cudaMemsetAsync(s->cell_mask, 0, sizeof(uint32_t) * s->cap, st));
   SP_CHECK(cudaMemsetAsync(s->tip, 0, sizeof(int) * 4, st));
   s->n_cells = 0;
+  s->cur_valid = false;
   return SP_OK;
 }
 
@@ -895,4 +1087,154 @@ extern "C" int sp_signal(int* dev_flag, int value, void* stream) {
 extern "C" int sp_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
   return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault,
                                      reinterpret_cast<cudaStream_t>(stream)));
+}
+
+// ---------------------------------------------------------------------------
+// K15 host side: one cooperative launch per draft request (draft.cu).
+// ---------------------------------------------------------------------------
+extern "C" int sp_stage_truncate(sp_stage* s, int n_cells) {
+  // position-addressed single-sequence stages (the draft): rows >= n_cells
+  // are discarded and will be overwritten by the next tokens
+  if (!s || n_cells < 0 || n_cells > s->n_cells) return SP_ERR_CACHE;
+  s->n_cells = n_cells;
+  s->cur_valid = false;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_feed, int pos0,
+                                     const int32_t* step_tokens, int steps, float cutoff,
+                                     sp_row_result* out, int* err_out, void* stream) {
+  if (!s || !out || n_feed < 0 || n_feed > DR_NT || steps < 0 || steps > DR_MAX_STEPS ||
+      (n_feed > 0 && !feed))
+    return SP_ERR_ARG;
+  const sp_model_dims& D = s->dims;
+  if (D.arch != SP_ARCH_LLAMA || D.w_dtype != SP_DTYPE_BF16 || s->tc || s->lo != 0 ||
+      s->hi != D.n_layers || !s->emb || !s->w_out || !s->final_norm || s->n_seq != 1 ||
+      (D.head_dim != 64 && D.head_dim != 128) || D.d_model % 8 || D.ffn_dim % 8 ||
+      D.d_model > 2048 || D.ffn_dim > 4096 || D.n_layers > DR_MAX_LAYERS)
+    return SP_ERR_ARG;
+  for (const LayerW& L : s->layers)
+    if (!L.qkv || !L.attn_norm || !L.mlp_norm) return SP_ERR_ARG;
+  if (pos0 != s->n_cells) return SP_ERR_PROTOCOL;   // rows == positions
+  const int total = n_feed + steps;
+  if (s->n_cells + total > s->cap || pos0 + total > D.max_context) return SP_ERR_CAPACITY;
+  for (int i = 0; i < n_feed; ++i)
+    if (feed[i] < 0 || feed[i] >= D.vocab) return SP_ERR_MODEL;
+  if (step_tokens)
+    for (int i = 0; i < steps; ++i)
+      if (step_tokens[i] < 0 || step_tokens[i] >= D.vocab) return SP_ERR_MODEL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int L = D.n_layers;
+  const int max_split = (s->cap + 127) / 128;
+  const size_t need = (size_t)DR_NT * D.n_heads * max_split * (D.head_dim + 2);
+  if (!s->dhdr) {
+    SP_CHECK(cudaMalloc((void**)&s->dxb, sizeof(float) * DR_NT * D.d_model));
+    SP_CHECK(cudaMalloc((void**)&s->dopart, sizeof(float) * DR_NT * D.n_heads * D.d_model));
+    SP_CHECK(cudaMalloc((void**)&s->dhdr, sizeof(DraftHdr)));
+    SP_CHECK(cudaMalloc((void**)&s->dbar, sizeof(unsigned)));
+    SP_CHECK(cudaMalloc((void**)&s->dlayers, sizeof(DraftLayer) * L));
+  }
+  if (need > s->att_scratch_floats) {
+    SP_CHECK(cudaStreamSynchronize(st));
+    drop_graphs(s);
+    cudaFree(s->att_scratch);
+    if (cudaMalloc((void**)&s->att_scratch, sizeof(float) * need) != cudaSuccess)
+      return SP_ERR_CUDA;
+    s->att_scratch_floats = need;
+  }
+  const int k = next_slot(s);
+  uint8_t* h = s->hdr_host + (size_t)k * s->hdr_bytes;
+  if (sizeof(DraftHdr) > s->hdr_bytes) return SP_ERR_CAPACITY;  // max_tokens too small
+  if (s->dlayers_dirty) {
+    // the layer table rides in the same pinned slot, after the header
+    DraftLayer* hl = reinterpret_cast<DraftLayer*>(h + sizeof(DraftHdr));
+    if (sizeof(DraftHdr) + sizeof(DraftLayer) * L > s->hdr_bytes) {
+      std::vector<DraftLayer> tmp(L);
+      for (int l = 0; l < L; ++l) {
+        const LayerW& W = s->layers[l];
+        tmp[l] = DraftLayer{(const __nv_bfloat16*)W.qkv, (const __nv_bfloat16*)W.o,
+                            (const __nv_bfloat16*)W.up, (const __nv_bfloat16*)W.down,
+                            W.attn_norm, W.mlp_norm};
+      }
+      SP_CHECK(cudaStreamSynchronize(st));
+      SP_CHECK(cudaMemcpy(s->dlayers, tmp.data(), sizeof(DraftLayer) * L,
+                          cudaMemcpyHostToDevice));
+    } else {
+      for (int l = 0; l < L; ++l) {
+        const LayerW& W = s->layers[l];
+        hl[l] = DraftLayer{(const __nv_bfloat16*)W.qkv, (const __nv_bfloat16*)W.o,
+                           (const __nv_bfloat16*)W.up, (const __nv_bfloat16*)W.down,
+                           W.attn_norm, W.mlp_norm};
+      }
+      SP_CHECK(cudaMemcpyAsync(s->dlayers, hl, sizeof(DraftLayer) * L, cudaMemcpyHostToDevice,
+                               st));
+    }
+    s->dlayers_dirty = false;
+  }
+  DraftHdr* hh = reinterpret_cast<DraftHdr*>(h);
+  std::memset(hh, 0, sizeof(DraftHdr));
+  hh->n_feed = n_feed;
+  hh->steps = steps;
+  hh->pos0 = pos0;
+  hh->row0 = s->n_cells;
+  hh->chain = step_tokens ? 0 : 1;
+  hh->cutoff = cutoff;
+  for (int i = 0; i < n_feed; ++i) hh->tok[i] = feed[i];
+  if (step_tokens)
+    for (int i = 0; i < steps; ++i) hh->tok[n_feed + i] = step_tokens[i];
+  SP_CHECK(cudaMemcpyAsync(s->dhdr, hh, sizeof(DraftHdr), cudaMemcpyHostToDevice, st));
+  SP_CHECK(cudaMemsetAsync(s->dbar, 0, sizeof(unsigned), st));
+  SP_CHECK(cudaEventRecord(s->ev[k], st));
+
+  DraftArgs a{};
+  a.layers = s->dlayers; a.L = L; a.V = D.vocab; a.d = D.d_model; a.H = D.n_heads;
+  a.KH = D.n_kv_heads; a.hd = D.head_dim; a.f = D.ffn_dim; a.eps = D.norm_eps;
+  a.theta = D.rope_theta;
+  a.emb = (const __nv_bfloat16*)s->emb; a.w_out = (const __nv_bfloat16*)s->w_out;
+  a.g_final = s->final_norm;
+  a.kc = (__nv_bfloat16*)s->kc; a.vc = (__nv_bfloat16*)s->vc;
+  a.kv_layer_elems = s->kv_layer_elems;
+  a.cell_pos = s->cell_pos; a.cell_mask = s->cell_mask;
+  a.hdr = s->dhdr; a.tip = s->tip; a.gate = s->gate;
+  a.x = s->xg; a.q = s->q; a.attn = s->attn; a.h = s->h;
+  a.att_part = s->att_scratch; a.att_tick = s->att_tickets; a.max_split = max_split;
+  a.lm_part = s->lm_scratch; a.bar = s->dbar;
+  a.xb = s->dxb; a.opart = s->dopart;
+  a.out = out; a.err = s->err; a.err_out = err_out;
+  if (getenv("SP_DRAFT_PROF")) {
+    if (!s->dprof) SP_CHECK(cudaMalloc((void**)&s->dprof, sizeof(long long) * 4096));
+    a.prof = s->dprof;
+  }
+  if (s->draft_ctas <= 0) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* env = getenv("SP_DRAFT_CTAS");
+    int want = env ? atoi(env) : sms;
+    if (want <= 0 || want > sms) want = sms;
+    draft_buffers(a, want);
+    if (draft_smem_bytes(a) > 200 * 1024) return SP_ERR_ARG;   // shape too wide
+    if (draft_max_ctas(a) < want) return SP_ERR_ARG;
+    s->draft_ctas = want;
+  }
+  draft_buffers(a, s->draft_ctas);
+  SP_CHECK(launch_draft_chain(a, s->draft_ctas, st));
+  s->n_cells += total;
+  s->cur_valid = false;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_draft_profile(sp_stage* s, long long* host, int max) {
+  // diagnostics: timestamps (ns) of the last decode_chain's phase edges
+  if (!s || !host || max <= 0) return SP_ERR_ARG;
+  if (!s->dprof) return 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -SP_ERR_CUDA;
+  long long n = 0;
+  if (cudaMemcpy(&n, s->dprof, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -SP_ERR_CUDA;
+  if (n > max) n = max;
+  if (cudaMemcpy(host, s->dprof + 1, sizeof(long long) * n, cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return -SP_ERR_CUDA;
+  return (int)n;
 }

@@ -346,7 +346,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
         reinterpret_cast<float*>(a.out)[(size_t)t * a.ldo + dim] = o;
       } else {
         __nv_bfloat16* cache = reinterpret_cast<__nv_bfloat16*>(sec == 1 ? a.k_cache : a.v_cache);
-        cache[(size_t)(a.cache_row0 + t) * a.kv_rows + dim] = __float2bfloat16_rn(o);
+        const int crow = a.cache_row0_dev ? *a.cache_row0_dev : a.cache_row0;
+        cache[(size_t)(crow + t) * a.kv_rows + dim] = __float2bfloat16_rn(o);
       }
     }
   } else if (EPI == SP_EPI_SWIGLU) {
@@ -487,7 +488,8 @@ int tc_ksplit(int n_rows, int k, int target_ctas) {
 // maps[1] the NT=128 one.
 cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st) {
   const int nt = tc_nt_for(a.m);
-  const int ksplit = a.ksplit > 0 ? a.ksplit : tc_ksplit(a.n_rows, a.k, 2 * 148);
+  const int budget = a.max_ctas > 0 ? a.max_ctas : 2 * 148;
+  const int ksplit = a.ksplit > 0 ? a.ksplit : tc_ksplit(a.n_rows, a.k, budget);
   for (int t0 = 0; t0 < a.m; t0 += nt) {
     a.tok0 = t0;
     cudaError_t e = nt == 16 ? launch_epi<16>(xmaps[0], a, ksplit, st)

@@ -60,7 +60,7 @@ class ControlPlane:
                  n_stat: int):
         from multiprocessing import shared_memory
         self.n_ranks = n_ranks
-        self.res_rows = 1 + n_stat + max_tokens
+        self.res_rows = 1 + max_tokens   # [status, err, -, -] + rows
         self.res_bytes = _align(self.res_rows * 16, 256)
         self.off_ring = PAGE
         self.off_cancel = self.off_ring + RING * SLOT
@@ -181,10 +181,9 @@ class _StageRank:
         d = model.config.embed_dim
         self.d = d
         self.words = max_tokens * d + 4
-        self.inbuf = torch.zeros((ACT_RING, self.words), dtype=torch.float32, device=model.device)
+        self.inbuf = torch.zeros(self.words, dtype=torch.float32, device=model.device)
         self.outbuf = torch.zeros((ACT_RING, self.words), dtype=torch.float32, device=model.device)
-        self.res = torch.zeros((RESULTS, plane.res_rows, 4), dtype=torch.int32,
-                               device=model.device)
+        self.gx_out = self.stage.io()[0]
         self.works = deque()
         torch.cuda.synchronize(model.device)
 
@@ -193,40 +192,39 @@ class _StageRank:
             self.works.popleft()
 
     def run(self, run_id, kind, flags, toks, rows) -> None:
+        """One stage-run as a graph-replayed ``sp_stage_step``.  The receive
+        buffer is fixed (NCCL's stream waits on this stream before writing
+        it, so the previous run has consumed it); the send goes from a ring
+        slot so a slow peer never holds up the next run's output."""
         import torch
         import torch.distributed as dist
         n = len(toks)
-        k = run_id % ACT_RING
         nw = n * self.d + 4
-        xin = self.inbuf[k]
-        xout = self.outbuf[k]
+        last = self.rank == self.world - 1
         with torch.cuda.stream(self.stream):
             if self.rank > 0:
-                dist.irecv(xin[:nw], src=self.rank - 1).wait()
-            self.stage.forward(toks, run_id, kind, flags,
-                               x_in=xin.data_ptr() if self.rank > 0 else None,
-                               in_status=xin[n * self.d:].data_ptr() if self.rank > 0 else None,
-                               x_out=xout.data_ptr(),
-                               out_status=xout[n * self.d:].data_ptr())
-            if self.rank < self.world - 1:
-                self.works.append(dist.isend(xout[:nw], dst=self.rank + 1))
+                dist.irecv(self.inbuf[:nw], src=self.rank - 1,
+                           group=_pair(self.rank - 1)).wait()
+            x_in = self.inbuf.data_ptr() if self.rank > 0 else None
+            stat = x_in + 4 * n * self.d if self.rank > 0 else None
+            slot = run_id % RESULTS
+            self.stage.step(toks, run_id, kind, flags, rows=rows if last else (),
+                            x_in=x_in, in_status=stat,
+                            res_copy=self.plane.res_dev(slot) if last and len(rows) else None)
+            s = self.stream.cuda_stream
+            if not last:
+                while len(self.works) >= ACT_RING - 1:   # slot reuse: its send is done
+                    self.works.popleft().wait()
+                xout = self.outbuf[run_id % ACT_RING]
+                check(self.stage.lib.sp_copy_async(xout.data_ptr(), self.gx_out, 4 * nw, s))
+                self.works.append(dist.isend(xout[:nw], dst=self.rank + 1,
+                                             group=_pair(self.rank)))
             else:
-                self._emit_result(run_id, n, rows, xout)
+                if not len(rows):  # status word only
+                    check(self.stage.lib.sp_copy_async(self.plane.res_dev(slot),
+                                                       self.gx_out + 4 * n * self.d, 4, s))
+                check(self.stage.lib.sp_signal(self.plane.flag_dev(slot), run_id, s))
         self._reap()
-
-    def _emit_result(self, run_id, n, rows, xout) -> None:
-        lib = self.stage.lib
-        slot = run_id % RESULTS
-        blk = self.res[slot]
-        s = self.stream.cuda_stream
-        # header: [status, err, n_rows, run_id]; stage status row; rows
-        check(lib.sp_copy_async(blk[0].data_ptr(), xout[n * self.d:].data_ptr(), 4, s))
-        if len(rows):
-            self.stage.lmhead(list(rows), x=xout.data_ptr(),
-                              out=blk[2:].data_ptr(), err_out=blk[0, 1:].data_ptr())
-        nbytes = 16 * (2 + len(rows))
-        check(lib.sp_copy_async(self.plane.res_dev(slot), blk.data_ptr(), nbytes, s))
-        check(lib.sp_signal(self.plane.flag_dev(slot), run_id, s))
 
     def copy(self, src, dst_mask, end) -> None:
         dsts = [i for i in range(32) if (dst_mask >> i) & 1]
@@ -328,7 +326,7 @@ class DistPipeline:
         err = int(blk[1])
         rows = []
         if status == _lib.SP_STATUS_VALID and nrow:
-            rr = blk[8:8 + 4 * nrow].view(RES_DTYPE).reshape(-1)
+            rr = blk[4:4 + 4 * nrow].view(RES_DTYPE).reshape(-1)
             rows = [RowResult(r["a"], r["b"], r["c"], r["d"]) for r in rr]
         return RunResult(run_id, status == _lib.SP_STATUS_PLACEHOLDER, rows, err,
                          [status] * self.world)
@@ -366,16 +364,29 @@ def init(max_tokens: int = 256):
     if not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     gloo = dist.new_group(backend="gloo")
+    # one NCCL communicator per adjacent pair: a rank's receive (from i-1)
+    # and send (to i+1) then run on different streams instead of being
+    # serialised as ops of one communicator
+    global _PAIRS
+    _PAIRS = [dist.new_group([i, i + 1], backend="nccl") for i in range(world - 1)]
     name = [f"sp_{os.getpid()}_{uuid.uuid4().hex[:8]}" if rank == 0 else None]
     dist.broadcast_object_list(name, src=0, group=gloo)
     n_stat = (world + 3) // 4
-    plane = ControlPlane(name[0], rank == 0, world, max_tokens, n_stat)
+    # rank 0 creates the segment; the others attach only after the barrier
+    plane = ControlPlane(name[0], True, world, max_tokens, n_stat) if rank == 0 else None
     dist.barrier(group=gloo)
     if rank != 0:
         plane = ControlPlane(name[0], False, world, max_tokens, n_stat)
     plane.register()
     dist.barrier(group=gloo)
     return rank, world, local, plane, gloo
+
+
+_PAIRS: list = []
+
+
+def _pair(i: int):
+    return _PAIRS[i] if 0 <= i < len(_PAIRS) else None
 
 
 def build_slice(cfg, rank: int, world: int, node_weights=None):
@@ -418,7 +429,7 @@ def bench_main(args):
         dist.destroy_process_group()
         return None
     dev = torch.device("cuda", local)
-    draft = build_model(cfg.draft_config(), dev)
+    draft = build_model(cfg.draft_config(), dev, tiled=cfg.draft_tc)
     pipe = DistPipeline(model, ranges, plane, world, cfg.partitions, cfg.capacity,
                         cfg.max_run_tokens)
     eng = Engine(cfg, target_model=model, draft_model=draft, pipeline=pipe)

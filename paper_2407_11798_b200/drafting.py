@@ -10,9 +10,11 @@ the draft's own CUDA stream; the head polls ``ready()`` and collects
 
 * ``ModelDraftServer`` — a real draft model (ToyDraft semantics).  The
   confidence test runs on the device: each step's LM head folds
-  ``conf >= cutoff`` into a gate word that the next step's kernels read, and
-  the next step's token is the previous argmax, so a whole micro-batch is
-  one stream of launches with a single readback.
+  ``conf >= cutoff`` into a gate that the next step reads, and the next
+  step's token is the previous argmax.  For llama bf16 drafts with
+  row-major weights the whole request (feed + chain) is ONE persistent
+  kernel (``sp_stage_decode_chain``, K15); otherwise one graph-replayed
+  ``sp_stage_step`` per forward.  Either way: one readback per request.
 * ``TableDraftServer`` — alpha-controlled synthetic proposals
   (SyntheticDraft, speculation.py:98-139): the target's greedy token with
   PCG64 probability alpha, else its runner-up, from a table of the target's
@@ -22,6 +24,7 @@ the draft's own CUDA stream; the head polls ``ready()`` and collects
 
 from __future__ import annotations
 
+import os
 from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
@@ -47,8 +50,21 @@ class _DraftBase:
             cap = capacity or max(1024, 8 * cfg.max_context)
             self.stage = Stage(draft_model, 0, cfg.n_layers, capacity=cap,
                                max_tokens=max_tokens, n_seq_ids=1, stream=self.stream)
-        self.res = torch.zeros((8, 4), dtype=torch.int32, device=draft_model.device)
-        self.res_host = torch.zeros((8, 4), dtype=torch.int32).pin_memory()
+        # result blocks: [status, err, -, -] + one row result (sp_stage_step);
+        # block 0 row = the chain's starting tip, 1..4 the chain steps, 7 feeds
+        self.res = torch.zeros((8, 2, 4), dtype=torch.int32, device=draft_model.device)
+        self.res_host = torch.zeros((8, 2, 4), dtype=torch.int32).pin_memory()
+        self._blocks: List[int] = []
+        cfgm = draft_model.config
+        self.fused_ok = (cfgm.arch == "llama" and cfgm.weight_dtype != "fp32"
+                         and not getattr(draft_model, "tiled", True)
+                         and cfgm.head_dim in (64, 128))
+        # the persistent kernel takes every SM: worth it when the draft has
+        # the GPU to itself (opt-in while it shares one with a target stage)
+        self.fused = self.fused_ok and os.environ.get("SP_DRAFT_FUSED") == "1"
+        # fused path: rows 0..64 of (argmax, second, conf, max_logit) + err word
+        self.rows = torch.zeros((66, 4), dtype=torch.int32, device=draft_model.device)
+        self.rows_host = torch.zeros((66, 4), dtype=torch.int32).pin_memory()
         self.event = torch.cuda.Event()
         self.tokens: List[int] = []
         self._pending = None
@@ -67,28 +83,71 @@ class _DraftBase:
 
     # -- shared GPU steps -------------------------------------------------------
     def _truncate(self, n: int) -> None:
+        """Rows == positions: drop tokens >= n and every cell past the kept
+        tokens (dead chain steps included)."""
         if n < len(self.tokens):
-            self.stage.cache_remove(0, n)
             self.stage.invalidate_tip()
             del self.tokens[n:]
+        self.stage.truncate(len(self.tokens))
+
+    def _launch_chain(self, feed: Sequence[int], pos0: int, steps: int, cutoff: float,
+                      step_tokens: Optional[Sequence[int]] = None) -> None:
+        """Fused request: feed + ``steps`` steps in one persistent launch;
+        results -> rows[0..steps], err -> rows[65, 0].  Feeds longer than the
+        kernel's 4-token tile (prefill) go through the batched path first."""
+        import torch
+        feed = list(feed)
+        if len(feed) > 4:
+            self._forward(feed, pos0)
+            pos0 += len(feed)
+            feed = []
+        self.stage.decode_chain(feed, pos0, steps, cutoff, self.rows.data_ptr(),
+                                self.rows[65].data_ptr(), step_tokens)
+        self.forwards += (1 if feed else 0) + steps
+        with torch.cuda.stream(self.stream):
+            self.rows_host.copy_(self.rows, non_blocking=True)
+            self.res_host.copy_(self.res, non_blocking=True)
+        self.event.record(self.stream)
+
+    def _chain(self, feed: Sequence[int], steps: int, cutoff: float) -> None:
+        self._launch_chain(feed, len(self.tokens), steps, cutoff)
+        self.tokens.extend(feed)
+
+    def _check_fused_err(self) -> None:
+        self._check_err()
+        err = int(self.rows_host[65, 0])
+        if err:
+            from . import _lib
+            _lib.raise_device_error(err, "draft")
 
     def _forward(self, toks: Sequence[int], base: int, chain: bool = False,
-                 update_tip: bool = True, gate: bool = False, cutoff: float = 0.0,
-                 out_row: Optional[int] = None) -> None:
+                 cutoff: float = 0.0, block: int = 7) -> None:
+        """One draft forward + LM head over its last token as one replayed
+        graph; result block -> ``res[block]``.  ``chain``: token 0 is the
+        previous argmax, gated on the device (conf >= cutoff)."""
+        from . import _lib
         batch = [BatchToken(t, base + i, frozenset([0]), i == len(toks) - 1)
                  for i, t in enumerate(toks)]
-        self.stage.forward(encode_tokens(batch), run_id=0, kind=KIND_CODE[PREFILL],
-                           flags=0, chain=chain)
-        out = self.res[out_row].data_ptr() if out_row is not None else self.res[7].data_ptr()
-        self.stage.lmhead([len(toks) - 1], out=out, err_out=self.res[6, 1:].data_ptr(),
-                          update_tip=update_tip, chain_gate=gate, cutoff=cutoff)
+        self.stage.step(encode_tokens(batch), run_id=0, kind=KIND_CODE[PREFILL], flags=0,
+                        rows=[len(toks) - 1],
+                        head=_lib.SP_STEP_CHAIN if chain else _lib.SP_STEP_TIP,
+                        cutoff=cutoff, res_copy=self.res[block].data_ptr())
         self.forwards += 1
+        self._blocks.append(block)
 
     def _finish_enqueue(self, nrows: int) -> None:
         import torch
         with torch.cuda.stream(self.stream):
             self.res_host.copy_(self.res, non_blocking=True)
         self.event.record(self.stream)
+
+    def _check_err(self) -> None:
+        blocks, self._blocks = self._blocks, []
+        for b in blocks:
+            err = int(self.res_host[b, 0, 1])
+            if err:
+                from . import _lib
+                _lib.raise_device_error(err, "draft")
 
     def ready(self) -> bool:
         return self._pending is not None and self.event.query()
@@ -106,32 +165,41 @@ class ModelDraftServer(_DraftBase):
             raise SpeculationError("draft request while one is in flight")
         self._truncate(truncate_to)
         feed = list(feed)
+        room = self.max_context - len(self.tokens) - len(feed)
+        budget = max(0, min(int(max_tokens), room, 4))
+        c32 = float(np.float32(cutoff))
+        if self.fused:
+            if feed or budget > 0:
+                self._chain(feed, budget, c32)
+            else:
+                self.event.record(self.stream)
+            self._pending = (budget, np.float32(cutoff), True)
+            return
         if feed:
             self._forward(feed, len(self.tokens))
             self.tokens.extend(feed)
-        room = self.max_context - len(self.tokens)
-        budget = max(0, min(int(max_tokens), room, 4))
-        c32 = float(np.float32(cutoff))
         if budget > 0:
-            self.stage.chain_begin(c32, self.res[0].data_ptr())
+            self.stage.chain_begin(c32, self.res[0, 1].data_ptr())
             base = len(self.tokens)
             for j in range(budget):
-                self._forward([0], base + j, chain=True, gate=True, cutoff=c32,
-                              out_row=1 + j)
+                self._forward([0], base + j, chain=True, cutoff=c32, block=1 + j)
         self._finish_enqueue(budget + 1)
-        self._pending = (budget, np.float32(cutoff))
+        self._pending = (budget, np.float32(cutoff), False)
 
     def reply(self) -> Tuple[tuple, tuple]:
-        budget, c32 = self._pending
+        budget, c32, fused = self._pending
         self.event.synchronize()
         self._pending = None
-        err = int(self.res_host[6, 1])
-        if err:
-            from . import _lib
-            _lib.raise_device_error(err, "draft")
+        if fused:
+            self._check_fused_err()
+        else:
+            self._check_err()
         if budget == 0:
             return (), ()
-        r = self.res_host[:budget + 1].numpy().view(RES_DTYPE).reshape(-1)
+        if fused:
+            r = self.rows_host[:budget + 1].numpy().view(RES_DTYPE).reshape(-1)
+        else:
+            r = self.res_host[:budget + 1, 1].numpy().view(RES_DTYPE).reshape(-1)
         toks, confs = [], []
         for j in range(budget):
             conf = np.float32(r[j]["c"])
@@ -183,13 +251,15 @@ class TableDraftServer(_DraftBase):
             else:
                 del self.tokens[truncate_to:]
             self.on_path = min(self.on_path, truncate_to)
+        elif self.charge:
+            self.stage.truncate(len(self.tokens))
         feed = list(feed)
+        feed_pos = len(self.tokens)
         if feed:
-            if self.charge:
-                self._forward(feed, len(self.tokens))
-            start = len(self.tokens)
+            if self.charge and not self.fused:
+                self._forward(feed, feed_pos)
             self.tokens.extend(feed)
-            self._retrack(start)
+            self._retrack(feed_pos)
         room = self.max_context - len(self.tokens)
         budget = max(0, min(int(max_tokens), room, 4))
         props = []
@@ -201,16 +271,25 @@ class TableDraftServer(_DraftBase):
                 best = self.truth[p] if p < len(self.truth) else 0
                 second = self.runner[p] if p < len(self.runner) else 1
                 tok = best if self.rng.random() < self.alpha else second
-                if self.charge:
+                if self.charge and not self.fused:
                     self._forward([tok], p)
                 self.tokens.append(tok)
                 self._retrack(p)
                 props.append(tok)
+        if self.charge and self.fused and (feed or props):
+            # the forwards a real draft would run, as one persistent launch
+            self._launch_chain(feed, feed_pos, len(props), 0.0, step_tokens=props)
+            self._pending = (tuple(props), True)
+            return
         self._finish_enqueue(1)
-        self._pending = tuple(props)
+        self._pending = (tuple(props), False)
 
     def reply(self) -> Tuple[tuple, tuple]:
-        props = self._pending
+        props, fused = self._pending
         self.event.synchronize()
         self._pending = None
+        if fused:
+            self._check_fused_err()
+        else:
+            self._check_err()
         return props, tuple(self.alpha for _ in props)

@@ -96,6 +96,10 @@ class ExperimentConfig:
     max_run_tokens: int = 256            # largest batch (prefill) per stage-run
     draft_charge: bool = True            # synthetic draft pays a real draft forward
                                          # per token (False ~ draft_token_delay=0)
+    draft_tc: bool = False               # llama draft on tcgen05 (True) or on the
+                                         # lower-latency CUDA-core GEMV path
+    draft_sm_reserve: int = 16           # SMs kept free of target GEMMs on the
+                                         # draft's GPU (so draft kernels start at once)
 
     def validate(self) -> None:
         if self.mode not in MODES:
@@ -857,13 +861,26 @@ class Engine:
         self.target = target_model or build_model(cfg.target_config(), self.device)
         self.draft_model = None
         if cfg.uses_draft():
-            self.draft_model = draft_model or build_model(cfg.draft_config(), self.device)
+            dc = cfg.draft_config()
+            self.draft_model = draft_model or build_model(
+                dc, self.device, tiled=(cfg.draft_tc if dc.arch == "llama" else None))
         ranges = plan_layer_split(self.target.config.n_layers, cfg.n_stages(), cfg.node_weights)
         self.pipe = pipeline or LocalPipeline(self.target, ranges, partitions=cfg.partitions,
                                               capacity=cfg.capacity,
                                               max_tokens=cfg.max_run_tokens)
         self.draft = None
-        self._draft_stream = torch.cuda.Stream(self.device) if cfg.uses_draft() else None
+        self._draft_stream = None
+        if cfg.uses_draft():
+            # the draft's tiny kernels must not queue behind the target's
+            # GEMMs on a shared GPU: highest stream priority + reserved SMs
+            hi = torch.cuda.Stream.priority_range()[1] if hasattr(
+                torch.cuda.Stream, "priority_range") else -1
+            self._draft_stream = torch.cuda.Stream(self.device, priority=hi)
+            if cfg.draft_sm_reserve > 0:
+                ctas = 2 * max(16, 148 - cfg.draft_sm_reserve)
+                for st in getattr(self.pipe, "stages", []):
+                    if st.device == self.device and st.cfg.arch == "llama":
+                        st.set_cta_budget(ctas)
         self._tables: Dict[int, tuple] = {}
 
     def _make_draft(self, prompt: List[int], prompt_seed: int):

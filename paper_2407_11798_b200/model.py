@@ -89,13 +89,16 @@ class ModelConfig:
     def eps(self) -> float:
         return 1e-8 if self.arch == "ref" else self.norm_eps
 
-    def dims(self) -> _lib.sp_model_dims:
+    def dims(self, tiled: Optional[bool] = None) -> _lib.sp_model_dims:
+        if tiled is None:
+            tiled = self.arch == "llama"
         return _lib.sp_model_dims(
             _lib.SP_ARCH_REF if self.arch == "ref" else _lib.SP_ARCH_LLAMA,
             self.vocab_size, self.embed_dim, self.n_layers, self.n_heads,
             self.kv_heads, self.head_dim, self.hidden, self.max_context,
             _lib.SP_DTYPE_F32 if self.weight_dtype == "fp32" else _lib.SP_DTYPE_BF16,
-            self.eps, self.rope_theta)
+            self.eps, self.rope_theta,
+            _lib.SP_LAYOUT_TC_TILED if tiled else _lib.SP_LAYOUT_NATURAL)
 
     def weight_bytes(self, layers: Optional[int] = None, head: bool = True,
                      embedding: bool = True) -> int:
@@ -350,14 +353,16 @@ def _ref_host_weights(config: ModelConfig) -> dict:
 
 def build_model(config: ModelConfig, device=None, layer_range=None,
                 embedding: Optional[bool] = None,
-                head: Optional[bool] = None) -> DeviceModel:
+                head: Optional[bool] = None, tiled: Optional[bool] = None) -> DeviceModel:
     """Seeded weights on the GPU (model.py:162-185).
 
     ref arch: the exact PCG64 float64 draws of the reference, stored fp32
     (or bf16) on the device.  llama arch: N(0,1)/sqrt(fan_in) with the
     residual-branch factor 1/sqrt(2L) (mirroring model.py:171-184), drawn on
     the device by a torch generator seeded per tensor, so every pipeline
-    rank can materialise just its own layers.
+    rank can materialise just its own layers.  ``tiled`` (llama default
+    True): store the layer weights in the tcgen05 tile layout; False keeps
+    them row-major for the CUDA-core GEMV path (small, latency-bound drafts).
     """
     import torch
 
@@ -369,6 +374,10 @@ def build_model(config: ModelConfig, device=None, layer_range=None,
     want_emb = (lo == 0) if embedding is None else embedding
     want_head = (hi == config.n_layers) if head is None else head
     m = DeviceModel(config, device, (lo, hi))
+    if tiled is not None:
+        if tiled and config.arch != "llama":
+            raise ModelError("tensor-core tiling needs the llama arch")
+        m.tiled = bool(tiled)
     tdt = torch.float32 if config.weight_dtype == "fp32" else torch.bfloat16
 
     def dev(a):
@@ -424,8 +433,9 @@ def build_model(config: ModelConfig, device=None, layer_range=None,
         up[0::2] = wg
         up[1::2] = wu
         del wg, wu
-        m.layers[l] = dict(qkv=tile_weight(torch.cat([wq, wk, wv], 0)), o=tile_weight(wo),
-                           up=tile_weight(up), down=tile_weight(wd), attn_norm=ones.clone(),
+        lay = tile_weight if m.tiled else (lambda t: t.contiguous())
+        m.layers[l] = dict(qkv=lay(torch.cat([wq, wk, wv], 0)), o=lay(wo),
+                           up=lay(up), down=lay(wd), attn_norm=ones.clone(),
                            mlp_norm=ones.clone())
         del wq, wk, wv, wo, up, wd
     if want_head:

@@ -57,16 +57,16 @@ class LocalPipeline:
                              cancel_table=self.cancel.data_ptr(),
                              cancel_size=cancel_size)
                        for lo, hi in ranges]
-        S = len(self.stages)
-        self.n_stat = (S + 3) // 4
-        rows = 1 + self.n_stat + max_tokens
-        self.res = torch.zeros((RESULT_RING, rows, 4), dtype=torch.int32, device=self.device)
-        self.res_host = torch.zeros((RESULT_RING, rows, 4), dtype=torch.int32).pin_memory()
+        # result block per in-flight run: [status, err, -, -] + rows
+        self.res_host = torch.zeros((RESULT_RING, 1 + max_tokens, 4),
+                                    dtype=torch.int32).pin_memory()
         self.res_np = self.res_host.numpy()
         self.events = [torch.cuda.Event() for _ in range(RESULT_RING)]
         torch.cuda.synchronize(self.device)
         self.fifo: deque = deque()
         self.max_tokens = max_tokens
+        self.d = model.config.embed_dim
+        self.io = [st.io() for st in self.stages]
 
     @property
     def n_stages(self) -> int:
@@ -83,30 +83,25 @@ class LocalPipeline:
     # -- transactions -----------------------------------------------------------
     def launch(self, run_id: int, kind: int, toks: np.ndarray, flags: int,
                rows: List[int]) -> None:
+        """Every stage's evaluation as one graph-replayed ``sp_stage_step``;
+        stage i reads stage i-1's fixed output buffer (activations + status
+        word), the last stage's result block lands in pinned host memory."""
         if len(self.fifo) >= RESULT_RING:
             raise RuntimeError("too many runs in flight")
+        if not rows:
+            raise ValueError("a run must request at least one logits row")
         slot = run_id % RESULT_RING
-        blk = self.res[slot]
-        prev = None
+        n = len(toks)
+        x_in = stat = None
+        last = len(self.stages) - 1
         for i, st in enumerate(self.stages):
-            stat = blk[1 + i // 4, i % 4:].data_ptr()
-            st.forward(toks, run_id, kind, flags,
-                       x_in=None if prev is None else prev.x.data_ptr(),
-                       in_status=None if prev is None else prev_stat,
-                       x_out=st.x.data_ptr(), out_status=stat)
-            prev, prev_stat = st, stat
-        last = self.stages[-1]
-        nrow = len(rows)
-        if nrow:
-            last.lmhead(rows, out=blk[1 + self.n_stat:].data_ptr(),
-                        err_out=blk[0, 1:].data_ptr())
-        nb = 1 + self.n_stat + nrow
-        import torch
-        with torch.cuda.stream(self.stream):
-            self.res_host[slot, :nb].copy_(blk[:nb], non_blocking=True)
-        ev = self.events[slot]
-        ev.record(self.stream)
-        self.fifo.append((run_id, slot, nrow))
+            st.step(toks, run_id, kind, flags, rows=rows if i == last else (),
+                    x_in=x_in, in_status=stat,
+                    res_copy=self.res_host[slot].data_ptr() if i == last else None)
+            x_in = self.io[i][0]
+            stat = x_in + 4 * n * self.d
+        self.events[slot].record(self.stream)
+        self.fifo.append((run_id, slot, len(rows)))
 
     def copy(self, src: int, dsts, end_pos: int) -> None:
         for st in self.stages:
@@ -127,14 +122,16 @@ class LocalPipeline:
     def _collect(self) -> RunResult:
         run_id, slot, nrow = self.fifo.popleft()
         blk = self.res_np[slot]
-        stats = blk[1:1 + self.n_stat].reshape(-1)[:self.n_stages].tolist()
-        placeholder = stats[-1] == _lib.SP_STATUS_PLACEHOLDER
+        status = int(blk[0, 0])
+        placeholder = status == _lib.SP_STATUS_PLACEHOLDER
         err = int(blk[0, 1])
         rows = []
         if not placeholder and nrow:
-            rr = blk[1 + self.n_stat:1 + self.n_stat + nrow].view(RES_DTYPE).reshape(-1)
+            rr = blk[1:1 + nrow].view(RES_DTYPE).reshape(-1)
             rows = [RowResult(r["a"], r["b"], r["c"], r["d"]) for r in rr]
-        return RunResult(run_id, placeholder, rows, err, stats)
+        # per-stage status is not read back: a placeholder anywhere reaches
+        # the last stage, which is what the head acts on
+        return RunResult(run_id, placeholder, rows, err, [status] * self.n_stages)
 
     def poll(self) -> Optional[RunResult]:
         return self._collect() if self.ready() else None

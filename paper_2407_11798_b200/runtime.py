@@ -43,7 +43,7 @@ class Stage:
         self.capacity, self.max_tokens, self.n_seq = capacity, max_tokens, n_seq_ids
         self.device = model.device
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self._dims = cfg.dims()
+        self._dims = cfg.dims(tiled=getattr(model, "tiled", None))
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             check(self.lib.sp_stage_create(C.byref(self._dims), lo, hi, capacity,
@@ -99,6 +99,11 @@ class Stage:
         ptr = table if isinstance(table, int) else table.data_ptr()
         check(self.lib.sp_stage_set_cancel_table(self.h, ptr, size))
 
+    def set_cta_budget(self, ctas: int) -> None:
+        """Cap the CTAs of this stage's tensor-core GEMMs (leaves SMs free
+        for a stream co-scheduled on the same GPU, e.g. the draft)."""
+        check(self.lib.sp_stage_set_cta_budget(self.h, int(ctas)))
+
     def n_cells(self) -> int:
         return self.lib.sp_stage_n_cells(self.h)
 
@@ -115,6 +120,44 @@ class Stage:
         check(rc, "sp_stage_forward")
         nl = (self.hi - self.lo) if layer_a < 0 else (layer_b - layer_a)
         self.launches += 5 * nl + (2 if flags & _lib.SP_FWD_CONTINUE else 4)
+
+    def step(self, toks: np.ndarray, run_id: int, kind: int, flags: int,
+             rows: Sequence[int] = (), head: int = 0, cutoff: float = 0.0,
+             x_in: Optional[int] = None, in_status: Optional[int] = None,
+             res_copy: Optional[int] = None) -> None:
+        """One whole stage-run (+ fused LM head over ``rows``) through the
+        graph-cached ``sp_stage_step``: outputs land in the stage's fixed
+        buffers (``io()``); the result block [status, err, -, -] + rows is
+        copied to ``res_copy`` (device or pinned host) when given."""
+        r = np.ascontiguousarray(rows, dtype=np.int32)
+        rc = self.lib.sp_stage_step(self.h, toks.ctypes.data, len(toks), run_id, kind, flags,
+                                    r.ctypes.data if len(r) else None, len(r), int(head),
+                                    float(cutoff), x_in, in_status, res_copy, self.s)
+        check(rc, "sp_stage_step")
+        self.launches += 5 * (self.hi - self.lo) + 4 + (2 if len(r) else 0)
+
+    def decode_chain(self, feed: Sequence[int], pos0: int, steps: int, cutoff: float,
+                     out: int, err_out: int, step_tokens: Optional[Sequence[int]] = None) -> None:
+        """A whole draft request in one persistent launch (K15): forward the
+        fed tokens, then ``steps`` chained (or given) single-token steps;
+        row results -> ``out[0..steps]``."""
+        f = np.ascontiguousarray(feed, dtype=np.int32)
+        st = None if step_tokens is None else np.ascontiguousarray(step_tokens, dtype=np.int32)
+        rc = self.lib.sp_stage_decode_chain(
+            self.h, f.ctypes.data if len(f) else None, len(f), int(pos0),
+            None if st is None else st.ctypes.data, int(steps), float(cutoff), out, err_out,
+            self.s)
+        check(rc, "sp_stage_decode_chain")
+        self.launches += 1
+
+    def truncate(self, n_cells: int) -> None:
+        check(self.lib.sp_stage_truncate(self.h, int(n_cells)), "sp_stage_truncate")
+
+    def io(self):
+        """(x_out, result block) device pointers written by ``step``."""
+        x, r = C.c_void_p(), C.c_void_p()
+        check(self.lib.sp_stage_io(self.h, C.byref(x), C.byref(r)), "sp_stage_io")
+        return x.value, r.value
 
     def lmhead(self, rows: Sequence[int], x: Optional[int] = None,
                out: Optional[int] = None, logits: Optional[int] = None,

@@ -10,8 +10,9 @@ import torch
 import paper_2407_11798_b200 as sp
 from paper_2407_11798_b200 import _lib
 
-cfg = sp.llama_config("llama2-7b")
-m = sp.build_model(cfg, layer_range=(0, 32), embedding=False, head=False)
+cfg = sp.llama_config(os.environ.get("SHAPE", "llama2-7b"))
+NL = cfg.n_layers
+m = sp.build_model(cfg, layer_range=(0, NL), embedding=False, head=False)
 lib = _lib.load()
 d, f = cfg.embed_dim, cfg.hidden
 X = torch.randn((256, f), device="cuda").to(torch.bfloat16)
@@ -49,7 +50,7 @@ def timed(fn, reps=5):
 for M in [int(x) for x in (sys.argv[1:] or ["1", "4", "16"])]:
     for name, (n, k) in kinds.items():
         ws = [m.layers[l][{"qkv": "qkv", "o": "o", "up": "up", "down": "down"}[name]]
-              for l in range(32)]
+              for l in range(NL)]
         a = _lib.sp_tc_args()
         a.n_rows, a.k, a.m, a.epi, a.norm = n, k, M, 0, 0
         a.out, a.ldo = out.data_ptr(), out.shape[1]
@@ -71,7 +72,7 @@ for M in [int(x) for x in (sys.argv[1:] or ["1", "4", "16"])]:
                 g.w = w.data_ptr()
                 _lib.check(lib.sp_gemv(C.byref(g), s))
 
-        byt = 32 * n * k * 2
+        byt = NL * n * k * 2
         t1, t2 = timed(tc), timed(cc)
-        print(f"M={M:3d} {name:5s} tc {t1*1e3/32:7.2f} us/launch {byt/t1/1e6:7.0f} GB/s | "
-              f"gemv {t2*1e3/32:7.2f} us {byt/t2/1e6:7.0f} GB/s", flush=True)
+        print(f"M={M:3d} {name:5s} tc {t1*1e3/NL:7.2f} us/launch {byt/t1/1e6:7.0f} GB/s | "
+              f"gemv {t2*1e3/NL:7.2f} us {byt/t2/1e6:7.0f} GB/s", flush=True)
