@@ -162,17 +162,22 @@ def gemv_roofline(engine, reps: int = 5) -> dict:
     import ctypes as C
     import torch
     from paper_2407_11798_b200 import _lib
-    st = engine.pipe.stages[0]
-    cfg, lib = st.cfg, st.lib
+    from paper_2407_11798_b200 import _lib as L_
+    stages = getattr(engine.pipe, "stages", [])
+    if stages:      # this rank's stage layers
+        st = stages[0]
+        cfg, lib, dev, layers = st.cfg, st.lib, st.device, range(st.lo, st.hi)
+    else:           # head + dedicated draft rank: the one-layer target shell
+        cfg, lib, dev = engine.target.config, L_.load(), engine.device
+        layers = sorted(engine.target.layers)
     d, f = cfg.embed_dim, cfg.hidden
     q, kv = cfg.n_heads * cfg.head_dim, cfg.kv_dim
-    dev = st.device
     X = torch.zeros((256, max(d, f)), device=dev, dtype=torch.bfloat16).normal_()
     out = torch.zeros((256, 2 * f + q + 2 * kv), device=dev, dtype=torch.float32)
     scratch = torch.zeros(8 << 20, device=dev)
     tick = torch.zeros(4096, dtype=torch.int32, device=dev)
     args, nbytes = [], 0
-    for l in range(st.lo, st.hi):
+    for l in layers:
         L = engine.target.layers[l]
         for key, n, k in (("qkv", q + 2 * kv, d), ("o", d, q), ("up", 2 * f, d),
                           ("down", d, f)):
@@ -292,10 +297,13 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, PCG64 prompts)",
         "config": {"workload": "configs[1]: Llama-2-7B-shape target + 160M-shape draft, "
-                               f"bf16, async-speculative (PipeInfer), {n_gpus}-stage pipeline",
+                               f"bf16, async-speculative (PipeInfer), "
+                               f"{eng.pipe.n_stages}-stage pipeline"
+                               + (", dedicated draft GPU" if eng.pipe.n_stages < n_gpus
+                                  else ", draft shares GPU 0"),
                    "target": TARGET, "draft": DRAFT, "alpha": ALPHA,
                    "prompt_len": PROMPT_LEN, "gen_len": args.gen_len,
-                   "pipeline_stages": n_gpus,
+                   "pipeline_stages": eng.pipe.n_stages,
                    "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
         "itl_ms": round(itl * 1e3, 3),
         "acceptance_rate": round(statistics.mean(r.metrics.acceptance_rate for r in res), 4),
@@ -355,6 +363,9 @@ def main():
     ap.add_argument("--gen-len", type=int, default=GEN_LEN)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--draft-gpu", action="store_true",
+                    help="N>1: rank 0 = head + dedicated draft GPU, stages on ranks 1..N-1 "
+                         "(the reference's nodes = stages + draft node)")
     args = ap.parse_args()
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None and int(os.environ.get("RANK", "0")) == 0:

@@ -124,12 +124,18 @@ struct DraftArgs {
   float* opart;        // [DR_NT, H, d] per-head O projections
   int bufA, bufD, bufE;  // per-CTA weight staging buffers (bytes)
   int kmax;
+  int ring_stages, ring_bytes;  // cluster form: weight ring per CTA
+  int nt;                       // cluster form: token rows of the activation buffers
 };
 
 size_t draft_smem_bytes(const DraftArgs& a);
 cudaError_t launch_draft_chain(const DraftArgs& a, int ctas, cudaStream_t st);
 int draft_max_ctas(const DraftArgs& a);
 void draft_buffers(DraftArgs& a, int ctas);
+size_t draft2_smem_bytes(const DraftArgs& a, int cl);
+size_t draft2_act_bytes(const DraftArgs& a, int cl, int nt);
+int draft2_cluster_size(const DraftArgs& a, int want);
+cudaError_t launch_draft_cluster(const DraftArgs& a, int cl, cudaStream_t st);
 
 cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
                         int n_old, int row0, const sp_token* toks, int n,

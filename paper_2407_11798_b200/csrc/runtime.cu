@@ -266,6 +266,8 @@ struct sp_stage {
   DraftHdr* dhdr = nullptr;
   unsigned* dbar = nullptr;
   int draft_ctas = 0;
+  int draft_cluster = 0;
+  int draft_stages = 0;
   long long* dprof = nullptr;            // SP_DRAFT_PROF: phase timestamps
   float* dxb = nullptr;
   float* dopart = nullptr;
@@ -1205,20 +1207,47 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
     if (!s->dprof) SP_CHECK(cudaMalloc((void**)&s->dprof, sizeof(long long) * 4096));
     a.prof = s->dprof;
   }
-  if (s->draft_ctas <= 0) {
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const char* env = getenv("SP_DRAFT_CTAS");
-    int want = env ? atoi(env) : sms;
-    if (want <= 0 || want > sms) want = sms;
-    draft_buffers(a, want);
-    if (draft_smem_bytes(a) > 200 * 1024) return SP_ERR_ARG;   // shape too wide
-    if (draft_max_ctas(a) < want) return SP_ERR_ARG;
-    s->draft_ctas = want;
+  const char* kind = getenv("SP_DRAFT_KERNEL");
+  if (kind && std::strcmp(kind, "grid") == 0) {
+    if (s->draft_ctas <= 0) {
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const char* env = getenv("SP_DRAFT_CTAS");
+      int want = env ? atoi(env) : sms;
+      if (want <= 0 || want > sms) want = sms;
+      draft_buffers(a, want);
+      if (draft_smem_bytes(a) > 200 * 1024) return SP_ERR_ARG;   // shape too wide
+      if (draft_max_ctas(a) < want) return SP_ERR_ARG;
+      s->draft_ctas = want;
+    }
+    draft_buffers(a, s->draft_ctas);
+    SP_CHECK(launch_draft_chain(a, s->draft_ctas, st));
+  } else {
+    // cluster form (default): one cluster of 16 (else 8) SMs
+    if (s->q_dim + 2 * s->kv_dim > D.ffn_dim) return SP_ERR_ARG;   // q|k|v staging in h
+    a.ring_bytes = 24 * 1024;
+    if ((long)a.ring_bytes < 2L * (D.ffn_dim > D.d_model ? D.ffn_dim : D.d_model) * 2)
+      a.ring_bytes = 4 * (D.ffn_dim > D.d_model ? D.ffn_dim : D.d_model);   // >= a row pair
+    const size_t budget = 200 * 1024;
+    if (s->draft_cluster <= 0) {
+      // size the ring for the widest launch (4 fed tokens) to pick the cluster
+      const size_t act4 = draft2_act_bytes(a, 16, DR_NT);
+      if (act4 + 2 * (size_t)a.ring_bytes > budget) return SP_ERR_ARG;   // shape too wide
+      a.ring_stages = (int)((budget - act4) / a.ring_bytes);
+      a.nt = DR_NT;
+      const char* env = getenv("SP_DRAFT_CLUSTER");
+      s->draft_cluster = draft2_cluster_size(a, env ? atoi(env) : 16);
+      if (s->draft_cluster <= 0) return SP_ERR_ARG;
+    }
+    // a launch with one fed token (every chain launch) gets a deeper ring
+    const int nt = n_feed > 1 ? n_feed : 1;
+    const size_t act = draft2_act_bytes(a, s->draft_cluster, nt);
+    a.ring_stages = (int)((budget - act) / a.ring_bytes);
+    if (a.ring_stages > 16) a.ring_stages = 16;
+    a.nt = nt;
+    SP_CHECK(launch_draft_cluster(a, s->draft_cluster, st));
   }
-  draft_buffers(a, s->draft_ctas);
-  SP_CHECK(launch_draft_chain(a, s->draft_ctas, st));
   s->n_cells += total;
   s->cur_valid = false;
   return SP_OK;

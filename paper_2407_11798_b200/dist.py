@@ -170,9 +170,10 @@ class _StageRank:
     """Per-rank stage state shared by the head side and the worker loop."""
 
     def __init__(self, model, lo, hi, rank, world, plane: ControlPlane, cfg_part,
-                 capacity, max_tokens):
+                 capacity, max_tokens, first: int = 0):
         import torch
         self.rank, self.world = rank, world
+        self.first = first          # rank of the first pipeline stage
         self.plane = plane
         self.stream = torch.cuda.Stream(model.device)
         self.stage = Stage(model, lo, hi, capacity=capacity, max_tokens=max_tokens,
@@ -201,12 +202,13 @@ class _StageRank:
         n = len(toks)
         nw = n * self.d + 4
         last = self.rank == self.world - 1
+        recv = self.rank > self.first
         with torch.cuda.stream(self.stream):
-            if self.rank > 0:
+            if recv:
                 dist.irecv(self.inbuf[:nw], src=self.rank - 1,
                            group=_pair(self.rank - 1)).wait()
-            x_in = self.inbuf.data_ptr() if self.rank > 0 else None
-            stat = x_in + 4 * n * self.d if self.rank > 0 else None
+            x_in = self.inbuf.data_ptr() if recv else None
+            stat = x_in + 4 * n * self.d if recv else None
             slot = run_id % RESULTS
             self.stage.step(toks, run_id, kind, flags, rows=rows if last else (),
                             x_in=x_in, in_status=stat,
@@ -235,10 +237,10 @@ class _StageRank:
 
 
 def worker_loop(model, lo, hi, rank, world, plane: ControlPlane, partitions,
-                capacity, max_tokens, on_mark=None) -> None:
+                capacity, max_tokens, on_mark=None, first: int = 0) -> None:
     """Ranks >= 1: serve control records until SHUTDOWN (never blocks on the GPU)."""
     import torch
-    sr = _StageRank(model, lo, hi, rank, world, plane, partitions, capacity, max_tokens)
+    sr = _StageRank(model, lo, hi, rank, world, plane, partitions, capacity, max_tokens, first)
     while True:
         rtype, p = plane.read(rank)
         if rtype == R_RUN:
@@ -266,26 +268,35 @@ class DistPipeline:
     """Head-side pipeline over torchrun ranks (rank 0 = head + stage 0)."""
 
     def __init__(self, model, ranges, plane: ControlPlane, world: int, partitions=8,
-                 capacity=8192, max_tokens=256):
+                 capacity=8192, max_tokens=256, local_stage: bool = True):
+        """``local_stage``: rank 0 hosts stage 0 (and the draft shares its
+        GPU); False: rank 0 is the head + dedicated draft node and the
+        stages live on ranks 1.. (the reference's n_stages = nodes - 1 with a
+        draft node, engine.py:171-176)."""
         self.plane = plane
         self.world = world
-        lo, hi = ranges[0]
-        self.sr = _StageRank(model, lo, hi, 0, world, plane, partitions, capacity,
-                             max_tokens)
-        self.stages = [self.sr.stage]
+        self.n_stage_ranks = len(ranges)
+        self.sr = None
+        self.stages = []
+        if local_stage:
+            lo, hi = ranges[0]
+            self.sr = _StageRank(model, lo, hi, 0, world, plane, partitions, capacity,
+                                 max_tokens)
+            self.stages = [self.sr.stage]
         self.fifo: deque = deque()
         self.n_stat = (world + 3) // 4
 
     @property
     def n_stages(self) -> int:
-        return self.world
+        return self.n_stage_ranks
 
     def reset(self) -> None:
         if self.fifo:
             raise RuntimeError("reset with runs in flight")
         self.plane.write(R_RESET, b"")
-        self.sr.stage.reset()
-        self.sr.stream.synchronize()
+        if self.sr is not None:
+            self.sr.stage.reset()
+            self.sr.stream.synchronize()
         self.plane.cancel[:] = 0
         self.plane.flags[:] = 0
 
@@ -296,7 +307,8 @@ class DistPipeline:
         if len(self.fifo) >= RESULTS:
             raise RuntimeError("too many runs in flight")
         self.plane.write(R_RUN, _pack_run(run_id, kind, flags, toks, rows))
-        self.sr.run(run_id, kind, flags, toks, rows)
+        if self.sr is not None:
+            self.sr.run(run_id, kind, flags, toks, rows)
         self.fifo.append((run_id, len(rows)))
 
     def copy(self, src, dsts, end_pos) -> None:
@@ -304,11 +316,13 @@ class DistPipeline:
         for d in dsts:
             m |= 1 << int(d)
         self.plane.write(R_COPY, struct.pack("<iIi", src, m, end_pos))
-        self.sr.copy(src, m, end_pos)
+        if self.sr is not None:
+            self.sr.copy(src, m, end_pos)
 
     def remove(self, seq, from_pos) -> None:
         self.plane.write(R_REMOVE, struct.pack("<ii", seq, from_pos))
-        self.sr.remove(seq, from_pos)
+        if self.sr is not None:
+            self.sr.remove(seq, from_pos)
 
     def cancel_run(self, run_id: int) -> None:
         self.plane.cancel[run_id % CANCEL] = run_id
@@ -329,7 +343,7 @@ class DistPipeline:
             rr = blk[4:4 + 4 * nrow].view(RES_DTYPE).reshape(-1)
             rows = [RowResult(r["a"], r["b"], r["c"], r["d"]) for r in rr]
         return RunResult(run_id, status == _lib.SP_STATUS_PLACEHOLDER, rows, err,
-                         [status] * self.world)
+                         [status] * self.n_stage_ranks)
 
     def poll(self) -> Optional[RunResult]:
         return self._collect() if self.ready() else None
@@ -346,7 +360,8 @@ class DistPipeline:
 
     def shutdown(self) -> None:
         self.plane.write(R_SHUTDOWN, b"")
-        self.sr.stream.synchronize()
+        if self.sr is not None:
+            self.sr.stream.synchronize()
 
 
 # ---------------------------------------------------------------------------
@@ -389,15 +404,21 @@ def _pair(i: int):
     return _PAIRS[i] if 0 <= i < len(_PAIRS) else None
 
 
-def build_slice(cfg, rank: int, world: int, node_weights=None):
-    """This rank's layer range and weights (plan_layer_split, engine.py:186-224)."""
+def build_slice(cfg, rank: int, world: int, node_weights=None, first: int = 0):
+    """This rank's layer range and weights (plan_layer_split, engine.py:186-224).
+    Stages live on ranks first..world-1; a rank below ``first`` (the head +
+    dedicated draft node) gets a one-layer shell of the target (its config and
+    the roofline probe's weights)."""
     import torch
     from .engine import plan_layer_split
     from .model import build_model
     tc = cfg.target_config()
-    ranges = plan_layer_split(tc.n_layers, world, node_weights)
+    ranges = plan_layer_split(tc.n_layers, world - first, node_weights)
     dev = torch.device("cuda", torch.cuda.current_device())
-    model = build_model(tc, dev, layer_range=ranges[rank])
+    if rank < first:
+        model = build_model(tc, dev, layer_range=(0, 1), embedding=False, head=False)
+    else:
+        model = build_model(tc, dev, layer_range=ranges[rank - first])
     return model, ranges
 
 
@@ -409,18 +430,28 @@ def bench_main(args):
     import bench as B
     from .engine import Engine, ExperimentConfig
     from .model import build_model, sample_prompt
-    cfg = ExperimentConfig(mode="async-speculative", nodes=world + 1,
+    # dedicated draft node: rank 0 = head + draft (the persistent draft kernel
+    # gets the whole GPU), stages on ranks 1.. -- the reference's layout
+    # (n_stages = nodes - 1); otherwise every rank hosts a stage and the draft
+    # shares rank 0's GPU
+    dedicated = bool(getattr(args, "draft_gpu", False)) and world >= 2
+    first = 1 if dedicated else 0
+    if dedicated and rank == 0:
+        os.environ.setdefault("SP_DRAFT_FUSED", "1")
+        os.environ.setdefault("SP_DRAFT_KERNEL", "grid")
+    cfg = ExperimentConfig(mode="async-speculative", nodes=world if dedicated else world + 1,
                            target_shape=B.TARGET, draft_shape=B.DRAFT,
                            draft_backend="synthetic", alpha=B.ALPHA,
                            prompt_len=B.PROMPT_LEN, gen_len=args.gen_len,
                            max_context=B.MAX_CTX, target_seed=1, draft_seed=2,
                            capacity=8192, node_weights=getattr(args, "node_weights", None))
-    model, ranges = build_slice(cfg, rank, world, cfg.node_weights)
+    model, ranges = build_slice(cfg, rank, world, cfg.node_weights, first)
     marks = []
     if rank != 0:
-        lo, hi = ranges[rank]
+        lo, hi = ranges[rank - first]
         worker_loop(model, lo, hi, rank, world, plane, cfg.partitions, cfg.capacity,
-                    cfg.max_run_tokens, on_mark=lambda t: marks.append((t, time.perf_counter())))
+                    cfg.max_run_tokens, on_mark=lambda t: marks.append((t, time.perf_counter())),
+                    first=first)
         out = [None]
         t = {m: v for m, v in marks}
         dist.gather_object((t.get(1), t.get(2)), None, dst=0, group=gloo)
@@ -431,7 +462,7 @@ def bench_main(args):
     dev = torch.device("cuda", local)
     draft = build_model(cfg.draft_config(), dev, tiled=cfg.draft_tc)
     pipe = DistPipeline(model, ranges, plane, world, cfg.partitions, cfg.capacity,
-                        cfg.max_run_tokens)
+                        cfg.max_run_tokens, local_stage=not dedicated)
     eng = Engine(cfg, target_model=model, draft_model=draft, pipeline=pipe)
     line = B.measure(eng, args, n_gpus=world, pipe=pipe)
     pipe.shutdown()

@@ -24,6 +24,10 @@ SHAPES = {
                   n_kv_heads=2, ffn_dim=1024, max_context=512, seed=3),
     "mha128": dict(arch="llama", vocab_size=777, embed_dim=256, n_layers=2, n_heads=2,
                    ffn_dim=768, max_context=512, seed=4),
+    # the 160M draft's widths (long down rows: 4-row ring chunks, parity ABA
+    # guard), two layers
+    "wide": dict(arch="llama", vocab_size=2000, embed_dim=768, n_layers=2, n_heads=12,
+                 ffn_dim=3072, max_context=512, seed=5),
 }
 
 
