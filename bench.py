@@ -224,6 +224,16 @@ def gemv_roofline(engine, reps: int = 5) -> dict:
 
 # ---------------------------------------------------------------------------
 
+def bench_knobs(args) -> dict:
+    """Engine knobs the run overrides (the reference's defaults otherwise)."""
+    kw = {}
+    for k in ("microbatch", "partitions", "cutoff"):
+        v = getattr(args, k, None)
+        if v is not None:
+            kw[k] = v
+    return kw
+
+
 def run_ours(args) -> dict:
     import torch
     from paper_2407_11798_b200.engine import Engine, ExperimentConfig
@@ -235,7 +245,8 @@ def run_ours(args) -> dict:
     cfg = ExperimentConfig(mode="async-speculative", nodes=2, target_shape=TARGET,
                            draft_shape=DRAFT, draft_backend="synthetic", alpha=ALPHA,
                            prompt_len=PROMPT_LEN, gen_len=args.gen_len, max_context=MAX_CTX,
-                           target_seed=1, draft_seed=2, capacity=8192)
+                           target_seed=1, draft_seed=2, capacity=8192,
+                           **bench_knobs(args))
     return measure(Engine(cfg), args, n_gpus=1)
 
 
@@ -304,6 +315,10 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
                    "target": TARGET, "draft": DRAFT, "alpha": ALPHA,
                    "prompt_len": PROMPT_LEN, "gen_len": args.gen_len,
                    "pipeline_stages": eng.pipe.n_stages,
+                   "engine": {"microbatch": eng.cfg.microbatch, "partitions": eng.cfg.partitions,
+                              "cutoff": eng.cfg.cutoff, "draft_kernel":
+                              os.environ.get("SP_DRAFT_KERNEL", "cluster")
+                              if os.environ.get("SP_DRAFT_FUSED", "1") != "0" else "per-forward"},
                    "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
         "itl_ms": round(itl * 1e3, 3),
         "acceptance_rate": round(statistics.mean(r.metrics.acceptance_rate for r in res), 4),
@@ -363,9 +378,13 @@ def main():
     ap.add_argument("--gen-len", type=int, default=GEN_LEN)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--draft-gpu", action="store_true",
+    ap.add_argument("--microbatch", type=int, default=None)
+    ap.add_argument("--partitions", type=int, default=None)
+    ap.add_argument("--cutoff", type=float, default=None)
+    ap.add_argument("--draft-gpu", default="auto", choices=["auto", "on", "off"],
                     help="N>1: rank 0 = head + dedicated draft GPU, stages on ranks 1..N-1 "
-                         "(the reference's nodes = stages + draft node)")
+                         "(the reference's nodes = stages + draft node); auto = on for N>=4 "
+                         "(measured: the shared layout wins at N=2, the dedicated one at N=4)")
     args = ap.parse_args()
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None and int(os.environ.get("RANK", "0")) == 0:

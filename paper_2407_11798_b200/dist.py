@@ -434,7 +434,8 @@ def bench_main(args):
     # gets the whole GPU), stages on ranks 1.. -- the reference's layout
     # (n_stages = nodes - 1); otherwise every rank hosts a stage and the draft
     # shares rank 0's GPU
-    dedicated = bool(getattr(args, "draft_gpu", False)) and world >= 2
+    mode = getattr(args, "draft_gpu", "off")
+    dedicated = world >= 2 and (mode == "on" or (mode == "auto" and world >= 4))
     first = 1 if dedicated else 0
     if dedicated and rank == 0:
         os.environ.setdefault("SP_DRAFT_FUSED", "1")
@@ -444,7 +445,8 @@ def bench_main(args):
                            draft_backend="synthetic", alpha=B.ALPHA,
                            prompt_len=B.PROMPT_LEN, gen_len=args.gen_len,
                            max_context=B.MAX_CTX, target_seed=1, draft_seed=2,
-                           capacity=8192, node_weights=getattr(args, "node_weights", None))
+                           capacity=8192, node_weights=getattr(args, "node_weights", None),
+                           **B.bench_knobs(args))
     model, ranges = build_slice(cfg, rank, world, cfg.node_weights, first)
     marks = []
     if rank != 0:

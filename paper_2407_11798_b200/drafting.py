@@ -59,9 +59,10 @@ class _DraftBase:
         self.fused_ok = (cfgm.arch == "llama" and cfgm.weight_dtype != "fp32"
                          and not getattr(draft_model, "tiled", True)
                          and cfgm.head_dim in (64, 128))
-        # the persistent kernel takes every SM: worth it when the draft has
-        # the GPU to itself (opt-in while it shares one with a target stage)
-        self.fused = self.fused_ok and os.environ.get("SP_DRAFT_FUSED") == "1"
+        # one persistent launch per request (K15): the cluster form (16 SMs)
+        # by default, the grid form (every SM) on a dedicated draft GPU;
+        # SP_DRAFT_FUSED=0 falls back to one graph-replayed step per forward
+        self.fused = self.fused_ok and os.environ.get("SP_DRAFT_FUSED", "1") != "0"
         # fused path: rows 0..64 of (argmax, second, conf, max_logit) + err word
         self.rows = torch.zeros((66, 4), dtype=torch.int32, device=draft_model.device)
         self.rows_host = torch.zeros((66, 4), dtype=torch.int32).pin_memory()
