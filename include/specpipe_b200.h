@@ -87,7 +87,11 @@ typedef struct sp_model_dims {
                           CUDA-core GEMV (latency-bound drafts)          */
 } sp_model_dims;
 
-enum { SP_LAYOUT_NATURAL = 0, SP_LAYOUT_TC_TILED = 1 };
+/* SWZ8: row-major bf16 rows whose 16-byte units are XOR-permuted within each
+ * 128-byte group, unit u of row r stored at u ^ (r & 7): a contiguous copy of
+ * any row block into shared memory is then bank-conflict-free for 8-row
+ * ldmatrix / LDS access (the persistent draft kernels); requires K % 64 == 0. */
+enum { SP_LAYOUT_NATURAL = 0, SP_LAYOUT_TC_TILED = 1, SP_LAYOUT_SWZ8 = 2 };
 
 /* One BatchToken (model.py:67-75); seq sets are bitmasks (P <= 32). */
 typedef struct sp_token {
@@ -156,6 +160,7 @@ typedef struct sp_gemv_args {
   const int* cancel_word;
   int32_t run_id;
   const int32_t* cache_row0_dev;  /* if set, overrides cache_row0 (run header) */
+  int32_t w_swz;          /* bf16 rows in the SWZ8 layout (see SP_LAYOUT_SWZ8) */
 } sp_gemv_args;
 
 int sp_gemv(const sp_gemv_args* a, void* stream);

@@ -28,7 +28,7 @@ SP_STATUS_VALID, SP_STATUS_PLACEHOLDER = 0, 1
 SP_FWD_CHECK_COVERAGE, SP_FWD_SKIPPABLE, SP_FWD_CONTINUE, SP_FWD_CHAIN = 1, 2, 4, 8
 SP_EPI_STORE, SP_EPI_RESID, SP_EPI_QKV, SP_EPI_GELU, SP_EPI_SWIGLU = range(5)
 SP_STEP_TIP, SP_STEP_CHAIN = 1, 2
-SP_LAYOUT_NATURAL, SP_LAYOUT_TC_TILED = 0, 1
+SP_LAYOUT_NATURAL, SP_LAYOUT_TC_TILED, SP_LAYOUT_SWZ8 = 0, 1, 2
 
 
 class sp_model_dims(C.Structure):
@@ -61,7 +61,7 @@ class sp_gemv_args(C.Structure):
                 ("head_dim", C.c_int32), ("rope_theta", C.c_float),
                 ("toks", C.c_void_p), ("err", C.c_void_p), ("run_state", C.c_void_p),
                 ("run_state_w", C.c_void_p), ("cancel_word", C.c_void_p),
-                ("run_id", C.c_int32), ("cache_row0_dev", C.c_void_p)]
+                ("run_id", C.c_int32), ("cache_row0_dev", C.c_void_p), ("w_swz", C.c_int32)]
 
 
 class sp_tc_args(C.Structure):

@@ -115,7 +115,7 @@ __device__ __forceinline__ void slice(int R, int& u0, int& u1) {
 // (ascending), then a butterfly: a fixed order.
 template <int NT, int R>
 __device__ __forceinline__ void warp_dot(const __nv_bfloat16* const (&w)[R], const float* xs,
-                                         int K, int n, float (&y)[R][NT]) {
+                                         int K, int n, float (&y)[R][NT], int row0g) {
   const int lane = threadIdx.x & 31;
   const int nch = K >> 3;
 #pragma unroll
@@ -130,7 +130,9 @@ __device__ __forceinline__ void warp_dot(const __nv_bfloat16* const (&w)[R], con
       const int c = c0 + 32 * u;
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        wv[u][r] = (c < nch && w[r]) ? ld_stream16(w[r] + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
+        wv[u][r] = (c < nch && w[r])
+                       ? ld_stream16(w[r] + (size_t)(c ^ ((row0g + r) & 7)) * 8)   // SWZ8
+                       : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -163,7 +165,7 @@ __device__ __forceinline__ void warp_dot(const __nv_bfloat16* const (&w)[R], con
 // copies ahead of the phase): no global round trip on the critical path.
 template <int NT, int R>
 __device__ __forceinline__ void warp_dot_s(const __nv_bfloat16* const (&w)[R], const float* xs,
-                                           int K, int n, float (&y)[R][NT]) {
+                                           int K, int n, float (&y)[R][NT], int row0g) {
   const int lane = threadIdx.x & 31;
   const int nch = K >> 3;
 #pragma unroll
@@ -175,7 +177,8 @@ __device__ __forceinline__ void warp_dot_s(const __nv_bfloat16* const (&w)[R], c
     float wf[R][8];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint4 u = w[r] ? *reinterpret_cast<const uint4*>(w[r] + (size_t)c * 8)
+      const uint4 u = w[r] ? *reinterpret_cast<const uint4*>(
+                                 w[r] + (size_t)(c ^ ((row0g + r) & 7)) * 8)   // SWZ8
                            : make_uint4(0, 0, 0, 0);
       bf16x8_to_f32(u, wf[r]);
     }
@@ -503,7 +506,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
           const __nv_bfloat16* const w2[2] = {bufA + (size_t)(2 * (u - qkv0)) * d,
                                               bufA + (size_t)(2 * (u - qkv0) + 1) * d};
           float y[2][DR_NT];
-          warp_dot_s<DR_NT, 2>(w2, xs, d, n, y);
+          warp_dot_s<DR_NT, 2>(w2, xs, d, n, y, 2 * u);
           if (lane < n) {
             const int m = lane;
             float y0 = 0.f, y1 = 0.f;
@@ -685,7 +688,8 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
 #pragma unroll
               for (int b = 0; b < OB; ++b) {
                 const int r = r0 + b * DR_WARPS * RW + rw;
-                wv[b] = r < d ? ld_stream16(Lw.o + (size_t)r * qd + hh * HD + lr * 8)
+                const int un = (hh * HD) / 8 + lr;            // SWZ8 unit of row r
+                wv[b] = r < d ? ld_stream16(Lw.o + (size_t)r * qd + (size_t)(un ^ (r & 7)) * 8)
                               : make_uint4(0, 0, 0, 0);
               }
               mark(65);
@@ -756,7 +760,8 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
             w6[2 * j + 1] = ok ? bufD + (size_t)(2 * (u + j - up0) + 1) * d : nullptr;
           }
           float y[6][DR_NT];
-          warp_dot_s<DR_NT, 6>(reinterpret_cast<const __nv_bfloat16* const(&)[6]>(w6), xs, d, n, y);
+          warp_dot_s<DR_NT, 6>(reinterpret_cast<const __nv_bfloat16* const(&)[6]>(w6), xs, d, n, y,
+                               2 * u);
           if (lane < n) {
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
@@ -803,7 +808,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
         const __nv_bfloat16* const w2[2] = {
             bufE + (size_t)(r - d0) * f, r + 1 < d1 ? bufE + (size_t)(r + 1 - d0) * f : nullptr};
         float y[2][DR_NT];
-        warp_dot_s<DR_NT, 2>(w2, xs, f, n, y);
+        warp_dot_s<DR_NT, 2>(w2, xs, f, n, y, r);
         if (lane < 2 * n) {
           const int m = lane >> 1, rr = r + (lane & 1);
           if (rr < d1) {
@@ -843,7 +848,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
 #pragma unroll
         for (int j = 0; j < 8; ++j) w8[j] = r + j < v1 ? a.w_out + (size_t)(r + j) * d : nullptr;
         float y[8][1];
-        warp_dot<1, 8>(reinterpret_cast<const __nv_bfloat16* const(&)[8]>(w8), xs, d, 1, y);
+        warp_dot<1, 8>(reinterpret_cast<const __nv_bfloat16* const(&)[8]>(w8), xs, d, 1, y, r);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           if (r + j >= v1) break;

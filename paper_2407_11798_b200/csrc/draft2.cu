@@ -98,7 +98,10 @@ struct K2Seg {
   const __nv_bfloat16* base;  // first row of this CTA's slice
   int rows;                   // rows in the slice
   int rb;                     // bytes per row
+  int rs;                     // bytes per row in the ring (= rb: the SWZ8 layout
+                              // keeps 8-row ldmatrix / LDS accesses conflict-free)
   int rc;                     // rows per chunk
+  int row0g;                  // matrix row of the slice's first row (SWZ8 key)
 };
 
 __device__ __forceinline__ K2Seg k2_seg(const DraftArgs& a, const DraftLayer* lw, int l, int ph,
@@ -110,20 +113,23 @@ __device__ __forceinline__ K2Seg k2_seg(const DraftArgs& a, const DraftLayer* lw
   if (ph == 0) {
     k2_slice((qd + 2 * kvd) / 2, rank, cl, u0, u1);
     s.base = lw[l].qkv + (size_t)2 * u0 * d; s.rows = 2 * (u1 - u0); s.rb = d * 2; pg = 2;
+    s.row0g = 2 * u0;
   } else if (ph == 1) {
     k2_slice(d, rank, cl, u0, u1);
-    s.base = lw[l].o + (size_t)u0 * qd; s.rows = u1 - u0; s.rb = qd * 2;
+    s.base = lw[l].o + (size_t)u0 * qd; s.rows = u1 - u0; s.rb = qd * 2; s.row0g = u0;
   } else if (ph == 2) {
     k2_slice(f, rank, cl, u0, u1);
     s.base = lw[l].up + (size_t)2 * u0 * d; s.rows = 2 * (u1 - u0); s.rb = d * 2; pg = 2;
+    s.row0g = 2 * u0;
   } else if (ph == 3) {
     k2_slice(d, rank, cl, u0, u1);
-    s.base = lw[l].down + (size_t)u0 * f; s.rows = u1 - u0; s.rb = f * 2;
+    s.base = lw[l].down + (size_t)u0 * f; s.rows = u1 - u0; s.rb = f * 2; s.row0g = u0;
   } else {
     k2_slice(a.V, rank, cl, u0, u1);
-    s.base = a.w_out + (size_t)u0 * d; s.rows = u1 - u0; s.rb = d * 2;
+    s.base = a.w_out + (size_t)u0 * d; s.rows = u1 - u0; s.rb = d * 2; s.row0g = u0;
   }
-  int rc = a.ring_bytes / s.rb;
+  s.rs = s.rb;
+  int rc = a.ring_bytes / s.rs;
   rc = rc / pg * pg;
   s.rc = rc < pg ? pg : rc;
   return s;
@@ -181,8 +187,9 @@ __device__ __forceinline__ int k2_row(int lane) {
   return r;
 }
 template <int R, int NT>
-__device__ __forceinline__ void k2_rows(const __nv_bfloat16* W, int nr, int K, const float* xs,
-                                        int ldx, int n, float (&res)[NT]) {
+__device__ __forceinline__ void k2_rows(const __nv_bfloat16* W, int ldw, int nr, int K,
+                                        const float* xs, int ldx, int n, float (&res)[NT],
+                                        int row0g) {
   const int lane = threadIdx.x & 31;
   const int nch = K >> 3;
   float acc[NT][R];
@@ -204,7 +211,8 @@ __device__ __forceinline__ void k2_rows(const __nv_bfloat16* W, int nr, int K, c
     uint4 wv[R];
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      wv[r] = r < nr ? *reinterpret_cast<const uint4*>(W + (size_t)r * K + (size_t)c * 8)
+      wv[r] = r < nr ? *reinterpret_cast<const uint4*>(
+                           W + (size_t)r * ldw + (size_t)(c ^ ((row0g + r) & 7)) * 8)   // SWZ8
                      : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -241,6 +249,67 @@ __device__ __forceinline__ void k2_rows(const __nv_bfloat16* W, int nr, int K, c
   }
 }
 
+// 16 weight rows (ring, padded stride ldw) x one token on the tensor cores:
+// mma.m16n8k16 with A = W rows (ldmatrix.x4), B = the token's activations
+// split into bf16 hi + lo parts (two MMAs, fp32 accumulate: ~2^-16 relative
+// to the fp32 product), column 0 of C = token 0.  Lanes with (lane & 3) == 0
+// return row lane/4 in r0 and row lane/4 + 8 in r1.  Hardware accumulation
+// order is fixed: deterministic.
+__device__ __forceinline__ void k2_mma_rows16(const __nv_bfloat16* W, int ldw, int nr, int K,
+                                              const __nv_bfloat16* xh, const __nv_bfloat16* xl,
+                                              float& r0, float& r1, int row0g) {
+  const int lane = threadIdx.x & 31;
+  const int t = lane & 3;
+  const bool col0 = lane < 4;   // only B column 0 (token 0) is non-zero
+  const int arow = min(lane & 15, nr - 1);
+  const uint32_t rbase = k2_s(W + (size_t)arow * ldw);
+  const int rx = (row0g + arow) & 7;   // SWZ8: unit u of this row sits at u ^ rx
+  const int uh = lane >> 4;            // this lane's 8-column half of the k-step
+  float ch[4] = {0.f, 0.f, 0.f, 0.f}, cl[4] = {0.f, 0.f, 0.f, 0.f};
+  // batches of KB k-steps: every shared-memory load of a batch is issued
+  // before its MMAs (asm volatile keeps source order, so the batching is
+  // what lets the loads overlap)
+  constexpr int KB = 4;
+  for (int kb = 0; kb < K; kb += 16 * KB) {
+    uint32_t af[KB][4], bf[KB][4];
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      const int k0 = kb + 16 * i;
+      if (k0 < K) {
+        const uint32_t pos = (uint32_t)(((k0 >> 3) + uh) ^ rx);
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(af[i][0]), "=r"(af[i][1]), "=r"(af[i][2]), "=r"(af[i][3])
+                     : "r"(rbase + pos * 16));
+      }
+      bf[i][0] = bf[i][1] = bf[i][2] = bf[i][3] = 0u;
+      if (col0 && k0 < K) {
+        bf[i][0] = *reinterpret_cast<const uint32_t*>(xh + k0 + 2 * t);
+        bf[i][1] = *reinterpret_cast<const uint32_t*>(xh + k0 + 8 + 2 * t);
+        bf[i][2] = *reinterpret_cast<const uint32_t*>(xl + k0 + 2 * t);
+        bf[i][3] = *reinterpret_cast<const uint32_t*>(xl + k0 + 8 + 2 * t);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      if (kb + 16 * i >= K) break;
+      asm volatile(
+          "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+          "{%8,%9}, {%0,%1,%2,%3};"
+          : "+f"(ch[0]), "+f"(ch[1]), "+f"(ch[2]), "+f"(ch[3])
+          : "r"(af[i][0]), "r"(af[i][1]), "r"(af[i][2]), "r"(af[i][3]), "r"(bf[i][0]),
+            "r"(bf[i][1]));
+      asm volatile(
+          "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+          "{%8,%9}, {%0,%1,%2,%3};"
+          : "+f"(cl[0]), "+f"(cl[1]), "+f"(cl[2]), "+f"(cl[3])
+          : "r"(af[i][0]), "r"(af[i][1]), "r"(af[i][2]), "r"(af[i][3]), "r"(bf[i][2]),
+            "r"(bf[i][3]));
+    }
+  }
+  r0 = __fadd_rn(ch[0], cl[0]);
+  r1 = __fadd_rn(ch[2], cl[2]);
+}
+
 struct K2Top2 { float v1; int i1; float v2; int i2; };
 __device__ __forceinline__ bool k2_better(float va, int ia, float vb, int ib) {
   return va > vb || (va == vb && ia < ib);
@@ -275,6 +344,9 @@ __global__ void __launch_bounds__(K2_THREADS, 1) draft_cluster_kernel(const Draf
   float* hbuf = abuf + NTR * qd;           // [NTR][f]   SwiGLU output (all rows)
   float* qkvb = hbuf + NTR * f;            // [HPC][NTR][3][HD] this CTA's heads' q, k, v
   float* lmp = qkvb + HPC * NTR * 3 * HD;  // [CL][8] LM-head partials of every CTA
+  const int KX = d > qd ? d : qd;
+  __nv_bfloat16* xh = reinterpret_cast<__nv_bfloat16*>(lmp + CL * 8);   // [KX] token-0 hi
+  __nv_bfloat16* xl = xh + KX;                                          // [KX] token-0 lo
 
   __shared__ __align__(8) uint64_t full[16], empty[16];
   __shared__ int sdone[16];
@@ -382,6 +454,46 @@ __global__ void __launch_bounds__(K2_THREADS, 1) draft_cluster_kernel(const Draf
   // ring stages) are in flight; a stage is released when all its parts are
   // done.  epi(row_in_slice, res) runs on the lanes that hold a row's sums.
   auto run_phase = [&](const K2Seg& sg, int K, const float* xs, int ldx, int n, auto&& epi) {
+    const int ldw = sg.rs / 2;
+    if (NT == 1 && sg.rc >= 16 && a.use_mma) {
+      // tensor-core path (opt-in, SP_DRAFT_MMA=1): one whole 16-row chunk per warp
+      const int nchunks = (sg.rows + sg.rc - 1) / sg.rc;
+      for (int c = warp; c < nchunks; c += K2_CW) {
+        const long g = ct + c;
+        const int st = (int)(g % a.ring_stages);
+        const long long t0 = clock64();
+        const int rnd = (int)(g / a.ring_stages);
+        for (uint32_t it = 0; srel[st] < rnd; ++it) {
+          __nanosleep(32);
+          if (it > (1u << 26)) __trap();
+        }
+        k2_wait(&full[st], (uint32_t)(rnd & 1));
+        wait_cyc += clock64() - t0;
+        const int crow = c * sg.rc;
+        const int rows_c = min(sg.rc, sg.rows - crow);
+        const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(
+            ring + (size_t)st * a.ring_bytes);
+        for (int h0 = 0; h0 < rows_c; h0 += 16) {
+          const int cnt = min(16, rows_c - h0);
+          float r0, r1;
+          k2_mma_rows16(W + (size_t)h0 * ldw, ldw, cnt, K, xh, xl, r0, r1, sg.row0g + crow + h0);
+          const bool lead = (lane & 3) == 0;
+          const int gr = lane >> 2;
+          float res0[NT], res1[NT];
+          res0[0] = r0;
+          res1[0] = r1;
+          epi(crow + h0 + gr, lead && gr < cnt, res0, 8);
+          epi(crow + h0 + 8 + gr, lead && 8 + gr < cnt, res1, 8);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          srel[st] = srel[st] + 1;
+          k2_arrive_local(&empty[st]);
+        }
+      }
+      ct += nchunks;
+      return;
+    }
     const int R = sg.rc >= 8 ? 8 : (sg.rc >= 4 ? 4 : 2);
     const int parts = (sg.rc + R - 1) / R;
     const int nchunks = (sg.rows + sg.rc - 1) / sg.rc;
@@ -406,12 +518,13 @@ __global__ void __launch_bounds__(K2_THREADS, 1) draft_cluster_kernel(const Draf
       const int r_lo = pt * R;
       const int cnt = min(R, rows_c - r_lo);
       const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(
-          ring + (size_t)st * a.ring_bytes) + (size_t)r_lo * K;
+          ring + (size_t)st * a.ring_bytes) + (size_t)r_lo * ldw;
       float res[NT];
       if (cnt > 0) {
-        if (R == 8) k2_rows<8, NT>(W, cnt, K, xs, ldx, n, res);
-        else if (R == 4) k2_rows<4, NT>(W, cnt, K, xs, ldx, n, res);
-        else k2_rows<2, NT>(W, cnt, K, xs, ldx, n, res);
+        const int rg = sg.row0g + crow + r_lo;
+        if (R == 8) k2_rows<8, NT>(W, ldw, cnt, K, xs, ldx, n, res, rg);
+        else if (R == 4) k2_rows<4, NT>(W, ldw, cnt, K, xs, ldx, n, res, rg);
+        else k2_rows<2, NT>(W, ldw, cnt, K, xs, ldx, n, res, rg);
         const int rr = R == 8 ? k2_row<8>(lane) : R == 4 ? k2_row<4>(lane) : k2_row<2>(lane);
         const bool owner = (lane & (32 / R - 1)) == 0;
         epi(crow + r_lo + rr, owner && rr < cnt, res, R);
@@ -475,6 +588,16 @@ __global__ void __launch_bounds__(K2_THREADS, 1) draft_cluster_kernel(const Draf
       }
     }
   };
+  // token-0 activations as bf16 hi + lo parts for the tensor-core GEMV
+  auto split_hilo = [&](const float* src, int K) {
+    if (NT != 1) return;
+    for (int k = tid; k < K; k += K2_CT) {
+      const float v = src[k];
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      xh[k] = h;
+      xl[k] = __float2bfloat16_rn(__fsub_rn(v, __bfloat162float(h)));
+    }
+  };
   auto stage_norm = [&](int n, const float* gain) {
     for (int m = 0; m < n; ++m)
       for (int k = tid * 4; k < d; k += K2_CT * 4) {
@@ -484,6 +607,8 @@ __global__ void __launch_bounds__(K2_THREADS, 1) draft_cluster_kernel(const Draf
             make_float4(__fmul_rn(v.x, g.x), __fmul_rn(v.y, g.y), __fmul_rn(v.z, g.z),
                         __fmul_rn(v.w, g.w));
       }
+    k2_cons_sync();
+    split_hilo(xn, d);
     k2_cons_sync();
   };
 
@@ -758,6 +883,8 @@ __global__ void __launch_bounds__(K2_THREADS, 1) draft_cluster_kernel(const Draf
       // ---------------- C: x += attn @ Wo (this CTA's rows) ------------------
       {
         const K2Seg sg = k2_seg(a, lw, l, 1, rank, CL);
+        split_hilo(abuf, qd);
+        k2_cons_sync();
         run_phase(sg, qd, abuf, qd, n, [&](int rs, bool own, float (&res)[NT], int) {
           if (!own) return;
           const int r = o0 + rs;
@@ -839,6 +966,8 @@ __global__ void __launch_bounds__(K2_THREADS, 1) draft_cluster_kernel(const Draf
             make_float4(__fmul_rn(v.x, g.x), __fmul_rn(v.y, g.y), __fmul_rn(v.z, g.z),
                         __fmul_rn(v.w, g.w));
       }
+      k2_cons_sync();
+      split_hilo(xn, d);
       k2_cons_sync();
       int v0, v1;
       k2_slice(a.V, rank, CL, v0, v1);
@@ -942,8 +1071,9 @@ __global__ void __launch_bounds__(K2_THREADS, 1) draft_cluster_kernel(const Draf
 size_t draft2_act_bytes(const DraftArgs& a, int cl, int nt) {
   const int qd = a.H * a.hd;
   const int hpc = (a.H + cl - 1) / cl;
+  const int kx = a.d > qd ? a.d : qd;
   return sizeof(float) * ((size_t)nt * (2 * a.d + qd + a.f) + (size_t)hpc * nt * 3 * a.hd +
-                          (size_t)cl * 8);
+                          (size_t)cl * 8) + 2 * sizeof(__nv_bfloat16) * (size_t)kx;
 }
 
 size_t draft2_smem_bytes(const DraftArgs& a, int cl) {

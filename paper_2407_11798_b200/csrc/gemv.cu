@@ -28,7 +28,7 @@ gemv_kernel(const sp_gemv_args a) {
   for (int mt0 = 0; mt0 < a.m; mt0 += MT) {
     const int mv = min(MT, a.m - mt0);
     gemv_core<T, MT, ROWS, NORM>(W, a.n_rows, a.k, a.x + (size_t)mt0 * a.ldx,
-                                 a.ldx, mv, a.gain, row0, sm);
+                                 a.ldx, mv, a.gain, row0, sm, a.w_swz);
     constexpr bool PAIRED = (EPI == SP_EPI_SWIGLU) || (EPI == SP_EPI_QKV);
     constexpr int PER = PAIRED ? 2 : 1;
     const int t = threadIdx.x;

@@ -34,7 +34,7 @@ __device__ __forceinline__ void gemv_core(const T* __restrict__ W, int n_rows,
                                           int ldx, int m_valid,
                                           const float* __restrict__ gain,
                                           int row0,
-                                          GemvSmem<T, MT, ROWS, NORM>& sm) {
+                                          GemvSmem<T, MT, ROWS, NORM>& sm, int swz = 0) {
   constexpr int VEC = VecTraits<T>::N;
   constexpr int CH = 32 * VEC;
   constexpr int U = (sizeof(T) == 2) ? 2 : 4;  // chunks in flight per lane
@@ -62,8 +62,11 @@ __device__ __forceinline__ void gemv_core(const T* __restrict__ W, int n_rows,
 #pragma unroll
       for (int r = 0; r < ROWS; ++r) {
         wv[u][r] = make_uint4(0, 0, 0, 0);
-        if (ok[u] && r < rvalid)
-          wv[u][r] = ld_stream16(W + (size_t)(row0 + r) * K + k);
+        if (ok[u] && r < rvalid) {
+          // SWZ8 (bf16): 16-byte unit k/8 of row R sits at (k/8) ^ (R & 7)
+          const int kk = swz ? ((((k >> 3) ^ ((row0 + r) & 7))) << 3) : k;
+          wv[u][r] = ld_stream16(W + (size_t)(row0 + r) * K + kk);
+        }
       }
     }
 #pragma unroll

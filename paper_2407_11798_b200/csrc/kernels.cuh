@@ -66,6 +66,7 @@ struct LmArgs {
   int* tip;         // device-side draft chain: [argmax, conf bits, valid]
   int* status_out;  // optional: run status (valid / placeholder)
   const RunHdr* hdr;  // optional: cutoff from the run header
+  int swz;            // weights in the SWZ8 layout
   int* gate;
   int chain_gate;
   float cutoff;
@@ -126,6 +127,7 @@ struct DraftArgs {
   int kmax;
   int ring_stages, ring_bytes;  // cluster form: weight ring per CTA
   int nt;                       // cluster form: token rows of the activation buffers
+  int use_mma;                  // cluster form: mma.sync GEMV for 16-row chunks
 };
 
 size_t draft_smem_bytes(const DraftArgs& a);

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) lmhead_kernel(const LmArgs a) {
     for (int mt0 = 0; mt0 < a.n_rows; mt0 += MT) {
       const int mv = min(MT, a.n_rows - mt0);
       gemv_core<T, MT, LM_ROWS, true>(W, a.V, a.d, a.x + (size_t)mt0 * a.d, a.d, mv,
-                                      a.norm ? a.gain : nullptr, row0, sm);
+                                      a.norm ? a.gain : nullptr, row0, sm, a.swz);
       if (threadIdx.x < mv) {
         const int m = threadIdx.x, mi = mt0 + m;
         const float sc = a.norm ? rms_scale(sm.ss[0][m], a.d, a.eps) : 1.0f;

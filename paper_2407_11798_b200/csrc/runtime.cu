@@ -211,6 +211,7 @@ struct sp_stage {
   int cancel_size = 0;
 
   bool tc = false;                       // bf16 llama path on tcgen05
+  int swz = 0;                           // row-major bf16 weights in SWZ8 layout
   int tc_ctas = 0;                       // CTA budget of the GEMMs (0 = all SMs)
   __nv_bfloat16* xb = nullptr;           // [mt, d]   normed input (x * gain)
   __nv_bfloat16* attnb = nullptr;        // [mt, q]   attention output
@@ -346,6 +347,14 @@ extern "C" int sp_stage_create(const sp_model_dims* dims, int layer_lo,
   if (d.w_layout == SP_LAYOUT_TC_TILED && !s->tc) {
     delete s;
     return SP_ERR_ARG;
+  }
+  if (d.w_layout == SP_LAYOUT_SWZ8) {
+    if (d.w_dtype != SP_DTYPE_BF16 || d.d_model % 64 || d.ffn_dim % 64 ||
+        (d.n_heads * d.head_dim) % 64) {
+      delete s;
+      return SP_ERR_ARG;
+    }
+    s->swz = 1;
   }
   if (s->tc && (d.d_model % 128 || s->q_dim % 128 || (s->q_dim + 2 * s->kv_dim) % 128 ||
                 d.ffn_dim % 64)) {
@@ -623,6 +632,7 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
       // ---- CUDA-core path (fp32 ref arch): weight-streaming GEMV ----
       sp_gemv_args g{};
       g.w_dtype = D.w_dtype;
+      g.w_swz = s->swz;
       g.run_state = s->run_state;
       g.err = s->err;
       g.toks = s->hdr_toks;
@@ -641,7 +651,8 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
       SP_CHECK(launch_attention(a, D.w_dtype, D.head_dim, st));
       // x += attn @ Wo (model.py:416)
       g = sp_gemv_args{};
-      g.w_dtype = D.w_dtype; g.run_state = s->run_state; g.err = s->err; g.toks = s->hdr_toks;
+      g.w_dtype = D.w_dtype; g.w_swz = s->swz; g.run_state = s->run_state; g.err = s->err;
+      g.toks = s->hdr_toks;
       g.m = n; g.w = L.o; g.n_rows = d; g.k = s->q_dim; g.x = s->attn; g.ldx = s->q_dim;
       g.norm = 0; g.epi = SP_EPI_RESID; g.out = x_out; g.ldo = d;
       rc = sp_gemv(&g, stream);
@@ -684,6 +695,7 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     m.gate = head->update_tip ? s->gate : nullptr;
     m.chain_gate = head->chain_gate;
     m.hdr = s->hdr;
+    m.swz = s->swz;
     SP_CHECK(launch_lmhead(m, D.w_dtype, st));
   }
   return SP_OK;
@@ -774,6 +786,7 @@ extern "C" int sp_stage_lmhead(sp_stage* s, const float* x,
   a.gate = update_tip ? s->gate : nullptr;
   a.chain_gate = chain_gate;
   a.hdr = s->hdr;
+  a.swz = s->swz;
   SP_CHECK(launch_lmhead(a, D.w_dtype, st));
   return SP_OK;
 }
@@ -1110,7 +1123,7 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
       (n_feed > 0 && !feed))
     return SP_ERR_ARG;
   const sp_model_dims& D = s->dims;
-  if (D.arch != SP_ARCH_LLAMA || D.w_dtype != SP_DTYPE_BF16 || s->tc || s->lo != 0 ||
+  if (D.arch != SP_ARCH_LLAMA || D.w_dtype != SP_DTYPE_BF16 || !s->swz || s->lo != 0 ||
       s->hi != D.n_layers || !s->emb || !s->w_out || !s->final_norm || s->n_seq != 1 ||
       (D.head_dim != 64 && D.head_dim != 128) || D.d_model % 8 || D.ffn_dim % 8 ||
       D.d_model > 2048 || D.ffn_dim > 4096 || D.n_layers > DR_MAX_LAYERS)
@@ -1226,9 +1239,14 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
   } else {
     // cluster form (default): one cluster of 16 (else 8) SMs
     if (s->q_dim + 2 * s->kv_dim > D.ffn_dim) return SP_ERR_ARG;   // q|k|v staging in h
-    a.ring_bytes = 24 * 1024;
-    if ((long)a.ring_bytes < 2L * (D.ffn_dim > D.d_model ? D.ffn_dim : D.d_model) * 2)
-      a.ring_bytes = 4 * (D.ffn_dim > D.d_model ? D.ffn_dim : D.d_model);   // >= a row pair
+    {   // a stage holds 16 padded rows of the short matrices (one tensor-core
+        // tile) and at least a pair of the long (down) rows
+      const long kx = s->q_dim > D.d_model ? s->q_dim : D.d_model;
+      long rb = 16 * (2 * kx);
+      const long rl = 2 * (2L * D.ffn_dim);
+      if (rl > rb) rb = rl;
+      a.ring_bytes = (int)((rb + 127) / 128 * 128);
+    }
     const size_t budget = 200 * 1024;
     if (s->draft_cluster <= 0) {
       // size the ring for the widest launch (4 fed tokens) to pick the cluster
@@ -1246,6 +1264,7 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
     a.ring_stages = (int)((budget - act) / a.ring_bytes);
     if (a.ring_stages > 16) a.ring_stages = 16;
     a.nt = nt;
+    a.use_mma = getenv("SP_DRAFT_MMA") && atoi(getenv("SP_DRAFT_MMA")) == 1;
     SP_CHECK(launch_draft_cluster(a, s->draft_cluster, st));
   }
   s->n_cells += total;

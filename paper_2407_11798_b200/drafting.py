@@ -58,6 +58,7 @@ class _DraftBase:
         cfgm = draft_model.config
         self.fused_ok = (cfgm.arch == "llama" and cfgm.weight_dtype != "fp32"
                          and not getattr(draft_model, "tiled", True)
+                         and getattr(draft_model, "swz", False)
                          and cfgm.head_dim in (64, 128))
         # one persistent launch per request (K15): the cluster form (16 SMs)
         # by default, the grid form (every SM) on a dedicated draft GPU;

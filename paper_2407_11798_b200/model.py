@@ -89,7 +89,7 @@ class ModelConfig:
     def eps(self) -> float:
         return 1e-8 if self.arch == "ref" else self.norm_eps
 
-    def dims(self, tiled: Optional[bool] = None) -> _lib.sp_model_dims:
+    def dims(self, tiled: Optional[bool] = None, swz: bool = False) -> _lib.sp_model_dims:
         if tiled is None:
             tiled = self.arch == "llama"
         return _lib.sp_model_dims(
@@ -98,7 +98,8 @@ class ModelConfig:
             self.kv_heads, self.head_dim, self.hidden, self.max_context,
             _lib.SP_DTYPE_F32 if self.weight_dtype == "fp32" else _lib.SP_DTYPE_BF16,
             self.eps, self.rope_theta,
-            _lib.SP_LAYOUT_TC_TILED if tiled else _lib.SP_LAYOUT_NATURAL)
+            _lib.SP_LAYOUT_TC_TILED if tiled else
+            (_lib.SP_LAYOUT_SWZ8 if swz else _lib.SP_LAYOUT_NATURAL))
 
     def weight_bytes(self, layers: Optional[int] = None, head: bool = True,
                      embedding: bool = True) -> int:
@@ -229,6 +230,7 @@ class DeviceModel:
         self.layers = {}          # layer -> dict of device tensors
         self.host = None
         self.tiled = config.arch == "llama"    # tensor-core weight layout
+        self.swz = False                        # row-major bf16 in the SWZ8 layout
         self._head_stage = None
 
     @property
@@ -257,10 +259,12 @@ class DeviceModel:
         f64 = lambda t: t.detach().float().cpu().numpy().astype(np.float64)  # noqa: E731
         out["embedding"] = f64(self.embedding) if self.embedding is not None else None
         out["pos_table"] = None if self.pos_table is None else f64(self.pos_table)
-        out["w_out"] = None if self.w_out is None else f64(self.w_out).T.copy()
+        w_out = self.w_out if (self.w_out is None or not self.swz) else swz8_weight(self.w_out)
+        out["w_out"] = None if w_out is None else f64(w_out).T.copy()
         out["final_norm"] = None if self.final_norm is None else f64(self.final_norm)
         lo, hi = self.layer_range
-        lay = (lambda t: untile_weight(t)) if self.tiled else (lambda t: t)
+        lay = (lambda t: untile_weight(t)) if self.tiled else (
+            (lambda t: swz8_weight(t)) if self.swz else (lambda t: t))
         for l in range(lo, hi):
             L = {k: (lay(v) if k in ("qkv", "o", "up", "down") else v)
                  for k, v in self.layers[l].items()}
@@ -301,6 +305,20 @@ def tile_weight(w):
         raise ModelError(f"tensor-core weights need N % 128 == 0 and K % 64 == 0, got {N}x{K}")
     t = w.reshape(N // 128, 128, K // 64, 8, 8).permute(0, 2, 1, 3, 4)
     return _swizzle_gather(t).contiguous().reshape(N, K)
+
+
+def swz8_weight(w):
+    """SWZ8 layout (include/specpipe_b200.h): unit u (8 bf16) of row r goes to
+    u ^ (r & 7).  An involution: applying it twice restores the rows."""
+    import torch
+    R, K = w.shape
+    assert K % 64 == 0, "SWZ8 needs K % 64 == 0"
+    w3 = w.reshape(R, K // 8, 8)
+    out = torch.empty_like(w3)
+    units = torch.arange(K // 8, device=w.device)
+    for j in range(8):
+        out[j::8] = w3[j::8][:, units ^ j]
+    return out.reshape(R, K).contiguous()
 
 
 def untile_weight(w):
@@ -433,13 +451,18 @@ def build_model(config: ModelConfig, device=None, layer_range=None,
         up[0::2] = wg
         up[1::2] = wu
         del wg, wu
-        lay = tile_weight if m.tiled else (lambda t: t.contiguous())
+        if not m.tiled and config.weight_dtype == "bf16" and d % 64 == 0 and f % 64 == 0 \
+                and (H * hd) % 64 == 0:
+            m.swz = True     # row-major for the CUDA-core / persistent draft kernels
+        lay = tile_weight if m.tiled else (swz8_weight if m.swz else (lambda t: t.contiguous()))
         m.layers[l] = dict(qkv=lay(torch.cat([wq, wk, wv], 0)), o=lay(wo),
                            up=lay(up), down=lay(wd), attn_norm=ones.clone(),
                            mlp_norm=ones.clone())
         del wq, wk, wv, wo, up, wd
     if want_head:
         m.w_out = draw(1, (config.vocab_size, d), 1 / math.sqrt(d))
+        if m.swz:
+            m.w_out = swz8_weight(m.w_out)
         m.final_norm = ones.clone()
     return m
 

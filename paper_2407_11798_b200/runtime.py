@@ -43,7 +43,7 @@ class Stage:
         self.capacity, self.max_tokens, self.n_seq = capacity, max_tokens, n_seq_ids
         self.device = model.device
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self._dims = cfg.dims(tiled=getattr(model, "tiled", None))
+        self._dims = cfg.dims(tiled=getattr(model, "tiled", None), swz=getattr(model, "swz", False))
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             check(self.lib.sp_stage_create(C.byref(self._dims), lo, hi, capacity,
