@@ -326,6 +326,10 @@ int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_feed, int pos0
 /* Position-addressed stages: drop rows >= n_cells (they are rewritten by the
  * next tokens; the draft's truncate, kvcache.py:120-149 for one sequence). */
 int sp_stage_truncate(sp_stage* s, int n_cells);
+/* Reclaim the rows of dead cells (stable compaction of the bounded cell
+ * pool; the reference's cache is unbounded).  Synchronises the stream;
+ * returns the new cell count or -error.  Not for position-addressed stages. */
+int sp_stage_compact(sp_stage* s, void* stream);
 /* Diagnostics (env SP_DRAFT_PROF=1): %globaltimer stamps of CTA 0 at every
  * phase edge of the last decode_chain; returns the count (or -error). */
 int sp_stage_draft_profile(sp_stage* s, long long* host, int max);

@@ -158,6 +158,10 @@ cudaError_t launch_copy(const int32_t* pos, uint32_t* mask, int n, int src,
 cudaError_t launch_remove(const int32_t* pos, uint32_t* mask, int n,
                           uint32_t seq_mask, int from_pos, cudaStream_t st);
 cudaError_t launch_keep(uint32_t* mask, int n, int seq, cudaStream_t st);
+cudaError_t launch_compact_scan(const int32_t* pos, const uint32_t* mask, int n, int32_t* src_of,
+                                int32_t* pos2, uint32_t* mask2, int* live, cudaStream_t st);
+cudaError_t launch_compact_gather(const void* src, void* dst, const int32_t* src_of,
+                                  const int* live, int row_bytes, int n_max, cudaStream_t st);
 bool make_map_bf16(CUtensorMap* map, const void* base, long rows, long cols, long ld_elems,
                    int box_rows);
 cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st);

@@ -81,6 +81,78 @@ cudaError_t launch_meta_write(int32_t* pos, uint32_t* mask, int row0,
   return cudaGetLastError();
 }
 
+// Stable compaction of the cell pool (reclaims rows of dead cells).  One
+// CTA scans the live flags (mask != 0) in row order: live row r gets the new
+// row new = #live rows before r, src_of[new] = r, and the metadata moves to
+// scratch (pos2/mask2) -> copied back by the host.  Row order among live
+// cells is preserved, so plan tie order (by row) and every result are
+// unchanged.
+__global__ void __launch_bounds__(KV_THREADS)
+compact_scan_kernel(const int32_t* __restrict__ pos, const uint32_t* __restrict__ mask, int n,
+                    int32_t* __restrict__ src_of, int32_t* __restrict__ pos2,
+                    uint32_t* __restrict__ mask2, int* live_out) {
+  __shared__ int wsum[KV_THREADS / 32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b = 0; b < n; b += KV_THREADS) {
+    const int r = b + threadIdx.x;
+    const int live = (r < n && mask[r] != 0u) ? 1 : 0;
+    int incl = live;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int base = carry;
+    for (int w = 0; w < warp; ++w) base += wsum[w];
+    if (live) {
+      const int nr = base + incl - 1;
+      src_of[nr] = r;
+      pos2[nr] = pos[r];
+      mask2[nr] = mask[r];
+    }
+    __syncthreads();
+    if (threadIdx.x == KV_THREADS - 1) carry = base + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *live_out = carry;
+}
+
+// gather the live K or V rows of one layer into scratch (new row order)
+__global__ void compact_gather_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                      const int32_t* __restrict__ src_of, const int* live,
+                                      int vec_per_row) {
+  const int nl = *live;
+  const long total = (long)nl * vec_per_row;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / vec_per_row), v = (int)(i % vec_per_row);
+    dst[i] = src[(size_t)src_of[r] * vec_per_row + v];
+  }
+}
+
+cudaError_t launch_compact_scan(const int32_t* pos, const uint32_t* mask, int n, int32_t* src_of,
+                                int32_t* pos2, uint32_t* mask2, int* live, cudaStream_t st) {
+  compact_scan_kernel<<<1, KV_THREADS, 0, st>>>(pos, mask, n, src_of, pos2, mask2, live);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact_gather(const void* src, void* dst, const int32_t* src_of,
+                                  const int* live, int row_bytes, int n_max, cudaStream_t st) {
+  const int vpr = row_bytes / 16;
+  long total = (long)n_max * vpr;
+  int grid = (int)((total + 255) / 256);
+  if (grid > 4 * 148) grid = 4 * 148;
+  if (grid < 1) grid = 1;
+  compact_gather_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(src),
+                                              reinterpret_cast<uint4*>(dst), src_of, live, vpr);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy(const int32_t* pos, uint32_t* mask, int n, int src,
                         uint32_t dst_mask, int end_pos, int max_context,
                         cudaStream_t st) {

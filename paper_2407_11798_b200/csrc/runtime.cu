@@ -272,6 +272,12 @@ struct sp_stage {
   long long* dprof = nullptr;            // SP_DRAFT_PROF: phase timestamps
   float* dxb = nullptr;
   float* dopart = nullptr;
+  // cell-pool compaction scratch (lazy)
+  int32_t* cp_src = nullptr;
+  int32_t* cp_pos = nullptr;
+  uint32_t* cp_mask = nullptr;
+  int* cp_live = nullptr;
+  void* cp_rows = nullptr;
 
   // last forward (split evaluation continues it)
   int cur_n = 0;
@@ -407,7 +413,8 @@ extern "C" int sp_stage_destroy(sp_stage* s) {
                   s->lm_scratch, s->lm_ticket, s->err, s->run_state, s->tip,
                   s->gate, s->hdr, s->xb, s->attnb, s->hb, s->ss,
                   s->tc_scratch, s->tc_tickets, s->gx_out, s->gres,
-                  s->dlayers, s->dhdr, s->dbar, s->dprof, s->dxb, s->dopart};
+                  s->dlayers, s->dhdr, s->dbar, s->dprof, s->dxb, s->dopart,
+                  s->cp_src, s->cp_pos, s->cp_mask, s->cp_live, s->cp_rows};
   for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->hdr_host) cudaFreeHost(s->hdr_host);
@@ -1285,4 +1292,54 @@ extern "C" int sp_stage_draft_profile(sp_stage* s, long long* host, int max) {
       cudaSuccess)
     return -SP_ERR_CUDA;
   return (int)n;
+}
+
+// ---------------------------------------------------------------------------
+// Cell-pool compaction: the reference's cache grows without bound; here the
+// pool is bounded, so dead cells (purged / removed runs) are reclaimed by a
+// stable compaction at a quiescent point of the stage's stream.  Synchronous:
+// returns the new cell count (>= 0) or -error.
+// ---------------------------------------------------------------------------
+extern "C" int sp_stage_compact(sp_stage* s, void* stream) {
+  if (!s) return -SP_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (s->n_cells == 0) return 0;
+  const size_t kvrow = wbytes(s->dims) * (size_t)s->kv_dim;
+  if (!s->cp_src) {
+    if (cudaMalloc((void**)&s->cp_src, sizeof(int32_t) * s->cap) != cudaSuccess ||
+        cudaMalloc((void**)&s->cp_pos, sizeof(int32_t) * s->cap) != cudaSuccess ||
+        cudaMalloc((void**)&s->cp_mask, sizeof(uint32_t) * s->cap) != cudaSuccess ||
+        cudaMalloc((void**)&s->cp_live, sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&s->cp_rows, kvrow * s->cap) != cudaSuccess)
+      return -SP_ERR_CUDA;
+  }
+  if (launch_compact_scan(s->cell_pos, s->cell_mask, s->n_cells, s->cp_src, s->cp_pos,
+                          s->cp_mask, s->cp_live, st) != cudaSuccess)
+    return -SP_ERR_CUDA;
+  int live = 0;
+  if (cudaMemcpyAsync(&live, s->cp_live, sizeof(int), cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+    return -SP_ERR_CUDA;
+  if (cudaMemcpyAsync(s->cell_pos, s->cp_pos, sizeof(int32_t) * live, cudaMemcpyDeviceToDevice,
+                      st) != cudaSuccess ||
+      cudaMemcpyAsync(s->cell_mask, s->cp_mask, sizeof(uint32_t) * live,
+                      cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+      cudaMemsetAsync(s->cell_mask + live, 0, sizeof(uint32_t) * (s->n_cells - live), st) !=
+          cudaSuccess)
+    return -SP_ERR_CUDA;
+  const int nl = s->hi - s->lo;
+  for (int l = 0; l < nl; ++l) {
+    for (int kv = 0; kv < 2; ++kv) {
+      char* base = (char*)(kv ? s->vc : s->kc) + wbytes(s->dims) * s->kv_layer_elems * l;
+      if (launch_compact_gather(base, s->cp_rows, s->cp_src, s->cp_live, (int)kvrow, live, st) !=
+              cudaSuccess ||
+          cudaMemcpyAsync(base, s->cp_rows, kvrow * live, cudaMemcpyDeviceToDevice, st) !=
+              cudaSuccess)
+        return -SP_ERR_CUDA;
+    }
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -SP_ERR_CUDA;
+  s->n_cells = live;
+  s->cur_valid = false;
+  return live;
 }

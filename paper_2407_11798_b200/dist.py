@@ -39,7 +39,7 @@ from .pipeline import RunResult
 from .runtime import RES_DTYPE, Stage
 
 # record types
-R_RUN, R_COPY, R_REMOVE, R_RESET, R_SHUTDOWN, R_MARK = 1, 2, 3, 4, 5, 6
+R_RUN, R_COPY, R_REMOVE, R_RESET, R_SHUTDOWN, R_MARK, R_COMPACT = 1, 2, 3, 4, 5, 6, 7
 
 RING = 2048            # control records
 SLOT = 4096            # bytes per record (header + <= 254 tokens)
@@ -252,6 +252,9 @@ def worker_loop(model, lo, hi, rank, world, plane: ControlPlane, partitions,
         elif rtype == R_RESET:
             sr.stage.reset()
             sr.stream.synchronize()
+        elif rtype == R_COMPACT:      # after every run queued before it
+            sr.stream.synchronize()
+            sr.stage.compact()
         elif rtype == R_MARK:
             sr.stream.synchronize()
             if on_mark is not None:
@@ -276,6 +279,9 @@ class DistPipeline:
         self.plane = plane
         self.world = world
         self.n_stage_ranks = len(ranges)
+        self.capacity = capacity
+        self.cells_since = 0       # cells appended on every stage since the last compaction
+        self.compactions = 0
         self.sr = None
         self.stages = []
         if local_stage:
@@ -294,6 +300,7 @@ class DistPipeline:
         if self.fifo:
             raise RuntimeError("reset with runs in flight")
         self.plane.write(R_RESET, b"")
+        self.cells_since = 0
         if self.sr is not None:
             self.sr.stage.reset()
             self.sr.stream.synchronize()
@@ -306,6 +313,16 @@ class DistPipeline:
     def launch(self, run_id, kind, toks, flags, rows) -> None:
         if len(self.fifo) >= RESULTS:
             raise RuntimeError("too many runs in flight")
+        if self.cells_since + len(toks) > self.capacity // 2:
+            # every stage reclaims its dead cells at this point of its record
+            # stream (live cells <= context + in-flight speculation)
+            self.plane.write(R_COMPACT, b"")
+            if self.sr is not None:
+                self.sr.stream.synchronize()
+                self.sr.stage.compact()
+            self.cells_since = 0
+            self.compactions += 1
+        self.cells_since += len(toks)
         self.plane.write(R_RUN, _pack_run(run_id, kind, flags, toks, rows))
         if self.sr is not None:
             self.sr.run(run_id, kind, flags, toks, rows)

@@ -67,6 +67,8 @@ class LocalPipeline:
         self.max_tokens = max_tokens
         self.d = model.config.embed_dim
         self.io = [st.io() for st in self.stages]
+        self.capacity = capacity
+        self.compactions = 0
 
     @property
     def n_stages(self) -> int:
@@ -92,6 +94,13 @@ class LocalPipeline:
             raise ValueError("a run must request at least one logits row")
         slot = run_id % RESULT_RING
         n = len(toks)
+        if self.stages[0].n_cells() + n > 0.75 * self.capacity:
+            # bounded cell pool: let the queued runs finish, then reclaim the
+            # dead cells (their results stay in the result ring for the head)
+            self.stream.synchronize()
+            for st in self.stages:
+                st.compact()
+            self.compactions += 1
         x_in = stat = None
         last = len(self.stages) - 1
         for i, st in enumerate(self.stages):

@@ -150,6 +150,13 @@ class Stage:
         check(rc, "sp_stage_decode_chain")
         self.launches += 1
 
+    def compact(self) -> int:
+        """Reclaim dead cells (stable; synchronises the stream); new count."""
+        rc = self.lib.sp_stage_compact(self.h, self.s)
+        if rc < 0:
+            check(-rc, "sp_stage_compact")
+        return rc
+
     def truncate(self, n_cells: int) -> None:
         check(self.lib.sp_stage_truncate(self.h, int(n_cells)), "sp_stage_truncate")
 

@@ -188,3 +188,46 @@ def test_device_draft_loop_matches_host_speculation(sp):
         props = sp.speculate_microbatch(st, max_tokens=4)
         assert list(toks) == [t for t, _ in props]
         assert np.allclose(confs, [c for _, c in props], rtol=1e-6)
+
+
+@pytest.mark.parametrize("seed", [5, 21])
+def test_bounded_cell_pool_compaction(sp, seed):
+    """A pool far smaller than the cells a generation appends: the pipeline
+    reclaims dead cells (stable compaction) and the stream still equals the
+    serial greedy decode."""
+    from paper_2407_11798_b200.engine import Engine
+    for mode, nodes in [("async-speculative", 4), ("sync-speculative", 3)]:
+        c = cfg(sp, mode=mode, nodes=nodes, prompt_seed=seed, gen_len=96, capacity=136,
+                partitions=3,
+                max_run_tokens=32, draft_backend="synthetic", alpha=0.5)
+        eng = Engine(c)
+        res = eng.run()
+        ref = sp.reference_decode(c.target_config(), sp.sample_prompt(seed, c.prompt_len,
+                                                                      c.vocab_size), 96)
+        assert res.tokens == ref, mode
+        assert eng.pipe.compactions > 0, mode
+
+
+def test_stage_compact_moves_live_rows(sp):
+    """Stage-level: compaction keeps live cells in row order with their K/V."""
+    import numpy as np
+    from paper_2407_11798_b200.runtime import Stage
+    from paper_2407_11798_b200.model import BatchToken, encode_tokens
+    c = sp.ModelConfig(vocab_size=64, embed_dim=32, n_layers=2, n_heads=2, max_context=256, seed=3)
+    m = sp.build_model(c)
+    st = Stage(m, 0, 2, capacity=64, max_tokens=16, n_seq_ids=4)
+    toks = [BatchToken(5 + i, i, frozenset([0]), i == 9) for i in range(10)]
+    st.forward(encode_tokens(toks), 0, 0, 0)
+    spec = [BatchToken(7, 10 + i, frozenset([1]), True) for i in range(4)]
+    st.forward(encode_tokens(spec), 1, 1, 0)
+    st.synchronize()
+    pos0, mask0 = st.meta_sync()
+    kv0 = {r: st.read_kv_sync(1, r) for r in range(14)}
+    st.cache_remove(1, 0)          # the speculative run's cells die
+    st.cache_remove(0, 6)          # and the tail of seq 0
+    assert st.compact() == 6
+    pos1, mask1 = st.meta_sync()
+    assert list(pos1[:6]) == list(pos0[:6]) and all(mask1[:6] == mask0[:6])
+    for r in range(6):
+        k, v = st.read_kv_sync(1, r)
+        assert np.array_equal(k, kv0[r][0]) and np.array_equal(v, kv0[r][1])
