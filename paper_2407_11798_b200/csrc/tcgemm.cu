@@ -282,26 +282,35 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
                  "r"(TMEM_COLS));
 
   if (nsplit > 1) {
-    // park the partial; the last CTA of this row tile merges in split order
-    float* part = a.scratch + ((size_t)tile * nsplit + split) * NT * TC_BM;
+    // split-K merge through distributed shared memory: the nsplit CTAs of
+    // this row tile form one cluster (grid y = cluster y); each parks its
+    // partial in its own (now idle) stage buffers, rank 0 sums them in split
+    // order straight from the peers' shared memory and runs the epilogue
+    float* part = reinterpret_cast<float*>(smem);          // [NT][TC_BM]
 #pragma unroll
     for (int c = 0; c < NT; ++c) part[c * TC_BM + row] = acc[c];
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0)
-      tail->last = (atomicAdd(&a.tickets[tile], 1) == nsplit - 1);
-    __syncthreads();
-    if (!tail->last) return;
-    __threadfence();
-    const float* base = a.scratch + (size_t)tile * nsplit * NT * TC_BM;
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    uint32_t crank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    if (crank == 0) {
+      const uint32_t la = smem_u32(part);
+      for (int sp2 = 1; sp2 < nsplit; ++sp2) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(sp2));
+        float v[NT];
 #pragma unroll
-    for (int c = 0; c < NT; ++c) acc[c] = ld_volatile_f(base + c * TC_BM + row);
-    for (int sp2 = 1; sp2 < nsplit; ++sp2) {
-      const float* p = base + (size_t)sp2 * NT * TC_BM;
+        for (int c = 0; c < NT; ++c)
+          asm volatile("ld.shared::cluster.f32 %0, [%1];"
+                       : "=f"(v[c]) : "r"(ra + (uint32_t)((c * TC_BM + row) * 4)));
 #pragma unroll
-      for (int c = 0; c < NT; ++c) acc[c] = __fadd_rn(acc[c], ld_volatile_f(p + c * TC_BM + row));
+        for (int c = 0; c < NT; ++c) acc[c] = __fadd_rn(acc[c], v[c]);
+      }
     }
-    if (threadIdx.x == 0) a.tickets[tile] = 0;
+    // peers keep their shared memory alive until rank 0 has read it
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (crank != 0) return;
   }
 
   // per-token RMSNorm scale from the producer's sum-of-squares partials
@@ -451,7 +460,21 @@ static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
     configured = true;
   }
   dim3 grid(a.n_rows / TC_BM, ksplit);
-  return launch_pdl(tc_gemm_kernel<NT, EPI, NORM>, grid, dim3(TC_THREADS), smem, st, x, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;   // the split-K CTAs of a tile
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = ksplit;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<NT, EPI, NORM>, x, a);
 }
 
 template <int NT>
@@ -481,7 +504,12 @@ int tc_nt_for(int m) { return m <= 16 ? 16 : 128; }
 // QKV 3, O 4, gate/up 1, down 9).
 int tc_ksplit(int n_rows, int k, int target_ctas) {
   const int tiles = n_rows / TC_BM, nchunk = k / TC_BK;
-  return max(1, min(target_ctas / tiles, nchunk / 16));
+  // the split CTAs of a tile merge as one cluster: at most 8 (portable size),
+  // a power of two (odd clusters schedule badly: measured QKV 18.5 us at 2,
+  // 26.5 at 3; O 11.0 at 4; down 18.7 at 8 on the 7B shapes)
+  int k = max(1, min(min(target_ctas / tiles, nchunk / 16), 8));
+  while (k & (k - 1)) k &= k - 1;
+  return k;
 }
 
 // Launch over all tokens (token tiles of NT); maps[0] is the NT=16 X map,
@@ -489,7 +517,8 @@ int tc_ksplit(int n_rows, int k, int target_ctas) {
 cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st) {
   const int nt = tc_nt_for(a.m);
   const int budget = a.max_ctas > 0 ? a.max_ctas : 2 * 148;
-  const int ksplit = a.ksplit > 0 ? a.ksplit : tc_ksplit(a.n_rows, a.k, budget);
+  int ksplit = a.ksplit > 0 ? a.ksplit : tc_ksplit(a.n_rows, a.k, budget);
+  if (ksplit > 8) ksplit = 8;
   for (int t0 = 0; t0 < a.m; t0 += nt) {
     a.tok0 = t0;
     cudaError_t e = nt == 16 ? launch_epi<16>(xmaps[0], a, ksplit, st)
