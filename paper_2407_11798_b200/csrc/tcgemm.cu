@@ -507,9 +507,9 @@ int tc_ksplit(int n_rows, int k, int target_ctas) {
   // the split CTAs of a tile merge as one cluster: at most 8 (portable size),
   // a power of two (odd clusters schedule badly: measured QKV 18.5 us at 2,
   // 26.5 at 3; O 11.0 at 4; down 18.7 at 8 on the 7B shapes)
-  int k = max(1, min(min(target_ctas / tiles, nchunk / 16), 8));
-  while (k & (k - 1)) k &= k - 1;
-  return k;
+  int ks = max(1, min(min(target_ctas / tiles, nchunk / 16), 8));
+  while (ks & (ks - 1)) ks &= ks - 1;
+  return ks;
 }
 
 // Launch over all tokens (token tiles of NT); maps[0] is the NT=16 X map,
