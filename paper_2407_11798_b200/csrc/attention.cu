@@ -116,7 +116,7 @@ plan_kernel(const int32_t* __restrict__ cell_pos,
 // fixed order (last-arriving CTA), so results do not depend on scheduling.
 // ---------------------------------------------------------------------------
 constexpr int ATT_THREADS = 128;
-constexpr int ATT_CH = 128;
+constexpr int ATT_CH = 32;   // plan entries per split: one load pass, K and V together
 constexpr int ATT_UNROLL = 4;
 
 
@@ -170,6 +170,10 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
   // context length; each split's partial is independent of which CTA ran it
   for (int s = blockIdx.z; s < ns; s += gridDim.z) {
     const int e0 = s * ATT_CH, e1 = min(len, e0 + ATT_CH);
+    // a split fits one pass for bf16 heads: its V rows are loaded together
+    // with its K rows (one round trip instead of two)
+    constexpr bool ONE = ATT_CH <= G * ATT_UNROLL;
+    uint4 vpre[ATT_UNROLL];
     // scores
     for (int eb = e0; eb < e1; eb += G * ATT_UNROLL) {
       uint4 kv[ATT_UNROLL];
@@ -178,6 +182,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
         const int e = eb + u * G + g;
         const int row = e < e1 ? plan[e] : plan[e0];
         kv[u] = ld_stream16(Kc + (size_t)row * kvd);
+        if (ONE) vpre[u] = ld_stream16(Vc + (size_t)row * kvd);
       }
 #pragma unroll
       for (int u = 0; u < ATT_UNROLL; ++u) {
@@ -224,9 +229,13 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
       uint4 vv[ATT_UNROLL];
 #pragma unroll
       for (int u = 0; u < ATT_UNROLL; ++u) {
-        const int e = eb + u * G + g;
-        const int row = e < e1 ? plan[e] : plan[e0];
-        vv[u] = ld_stream16(Vc + (size_t)row * kvd);
+        if (ONE) {
+          vv[u] = vpre[u];
+        } else {
+          const int e = eb + u * G + g;
+          const int row = e < e1 ? plan[e] : plan[e0];
+          vv[u] = ld_stream16(Vc + (size_t)row * kvd);
+        }
       }
 #pragma unroll
       for (int u = 0; u < ATT_UNROLL; ++u) {

@@ -56,7 +56,8 @@ __global__ void embed_kernel(const T* __restrict__ emb,
 __global__ void gate_kernel(const RunHdr* hdr, sp_token* toks, const int* cancel_table,
                             const int* in_status, const int* gate, const int* chain_tip,
                             int* run_state, int32_t* cell_pos, uint32_t* cell_mask,
-                            int n_seq, int max_context, int* err) {
+                            int n_seq, int max_context, int* err,
+                            unsigned long long cond) {
   pdl_wait();
   pdl_trigger();
   __shared__ int skip;
@@ -73,6 +74,9 @@ __global__ void gate_kernel(const RunHdr* hdr, sp_token* toks, const int* cancel
     if ((flags & SP_FWD_CHAIN) && chain_tip) toks[0].token = chain_tip[0];
     *run_state = s;
     skip = s;
+    // graph-replayed runs: the layers sit in a conditional node that a
+    // skipped run does not execute at all
+    if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, s ? 0u : 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -260,6 +264,8 @@ struct sp_stage {
   std::map<std::vector<long>, cudaGraphExec_t> graphs;
   std::map<std::vector<long>, int> seen;
   bool use_graphs = true;
+  bool use_cond = true;                  // conditional (IF) body in captured steps
+  cudaStream_t body_st = nullptr;
 
   // K15 draft chain (persistent kernel)
   DraftLayer* dlayers = nullptr;         // device copy of the layer table
@@ -394,6 +400,7 @@ extern "C" int sp_stage_create(const sp_model_dims* dims, int layer_lo,
   alloc((void**)&s->gx_out, sizeof(float) * ((size_t)mt * d.d_model + 4));
   alloc((void**)&s->gres, sizeof(sp_row_result) * (size_t)(mt + 1));
   s->use_graphs = getenv("SP_NO_GRAPHS") == nullptr;
+  s->use_cond = getenv("SP_NO_COND_GRAPH") == nullptr;
   for (int i = 0; ok && i < DESC_RING; ++i)
     if (cudaEventCreateWithFlags(&s->ev[i], cudaEventDisableTiming) != cudaSuccess) ok = false;
   if (ok) ok = cudaDeviceSynchronize() == cudaSuccess;
@@ -416,6 +423,7 @@ extern "C" int sp_stage_destroy(sp_stage* s) {
                   s->dlayers, s->dhdr, s->dbar, s->dprof, s->dxb, s->dopart,
                   s->cp_src, s->cp_pos, s->cp_mask, s->cp_live, s->cp_rows};
   for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
+  if (s->body_st) cudaStreamDestroy(s->body_st);
   for (void* p : ptrs) if (p) cudaFree(p);
   if (s->hdr_host) cudaFreeHost(s->hdr_host);
   for (int i = 0; i < DESC_RING; ++i) if (s->ev[i]) cudaEventDestroy(s->ev[i]);
@@ -529,16 +537,49 @@ struct HeadIO {            // fused LM head over the header's rows
 // captured once and replayed for any run of the same token count.
 static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
                        int max_pos, bool coverage, bool graphable, const RunIO& io,
-                       const HeadIO* head, cudaStream_t st) {
+                       const HeadIO* head, cudaStream_t st, cudaStream_t body_st = nullptr) {
   const sp_model_dims& D = s->dims;
   const int d = D.d_model;
-  void* stream = reinterpret_cast<void*>(st);
+  // body_st (capture only): the gate kernel is followed by an IF node whose
+  // body -- captured on body_st -- holds the layers; the epilogue and the
+  // LM head stay outside (a skipped run still purges and reports)
+  unsigned long long cond = 0;
+  cudaGraph_t cap_graph = nullptr;
+  if (body_st) {
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamGetCaptureInfo(st, &cs, nullptr, &cap_graph, nullptr, nullptr) != cudaSuccess ||
+        cs != cudaStreamCaptureStatusActive)
+      return SP_ERR_CUDA;
+    cudaGraphConditionalHandle h;
+    SP_CHECK(cudaGraphConditionalHandleCreate(&h, cap_graph, 0, 0));
+    cond = (unsigned long long)h;
+  }
   if (!cont) {
     SP_CHECK(launch_pdl(gate_kernel, dim3(1), dim3(128), 0, st, (const RunHdr*)s->hdr,
                         s->hdr_toks, s->cancel_table, io.in_status,
                         (const int*)s->gate, (const int*)s->tip, s->run_state, s->cell_pos,
-                        s->cell_mask, s->n_seq, D.max_context, s->err));
+                        s->cell_mask, s->n_seq, D.max_context, s->err, cond));
   }
+  cudaStream_t outer = st;
+  if (body_st) {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    SP_CHECK(cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = (cudaGraphConditionalHandle)cond;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    SP_CHECK(cudaGraphAddNode(&cn, cap_graph, deps, nd, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SP_CHECK(cudaStreamUpdateCaptureDependencies(st, &cn, 1, cudaStreamSetCaptureDependencies));
+    SP_CHECK(cudaStreamBeginCaptureToGraph(body_st, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    st = body_st;
+  }
+  void* stream = reinterpret_cast<void*>(st);
   if (layer_a == 0) {
     const int threads = d >= 256 ? 256 : 64;
     if (D.w_dtype == SP_DTYPE_BF16)
@@ -682,6 +723,11 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     if (s->cancel_table && l + 1 < layer_b && ((l + 1 - layer_a) % OBSERVE_EVERY) == 0)
       SP_CHECK(launch_pdl(observe_kernel, dim3(1), dim3(1), 0, st, (const RunHdr*)s->hdr,
                           s->cancel_table, s->run_state));
+  }
+  if (body_st) {
+    cudaGraph_t g;
+    SP_CHECK(cudaStreamEndCapture(body_st, &g));
+    st = outer;
   }
   SP_CHECK(launch_pdl(epilogue_kernel, dim3(max(1, min(148, (s->cap + 255) / 256))),
                       dim3(256), 0, st, (const RunHdr*)s->hdr, (const sp_token*)s->hdr_toks,
@@ -841,15 +887,40 @@ extern "C" int sp_stage_step(sp_stage* s, const sp_token* host_toks, int n, int 
     } else if (s->seen[key]++ == 0) {
       rc = enqueue_run(s, n, s->lo, s->hi, false, max_pos, true, true, io, &head, st);
     } else {
-      cudaGraph_t g;
-      SP_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      rc = enqueue_run(s, n, s->lo, s->hi, false, max_pos, true, true, io, &head, st);
-      cudaError_t e = cudaStreamEndCapture(st, &g);
-      if (rc) return rc;
-      SP_CHECK(e);
-      cudaGraphExec_t ex;
-      SP_CHECK(cudaGraphInstantiate(&ex, g, 0));
-      cudaGraphDestroy(g);
+      // capture; the layers go into a conditional (IF) node that the gate
+      // kernel switches off for a cancelled run (SP_NO_COND_GRAPH=1: plain)
+      cudaGraphExec_t ex = nullptr;
+      if (s->use_cond && !s->body_st &&
+          cudaStreamCreateWithFlags(&s->body_st, cudaStreamNonBlocking) != cudaSuccess)
+        s->use_cond = false;
+      for (int attempt = s->use_cond ? 0 : 1; attempt < 2 && !ex; ++attempt) {
+        cudaGraph_t g = nullptr;
+        SP_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue_run(s, n, s->lo, s->hi, false, max_pos, true, true, io, &head, st,
+                         attempt == 0 ? s->body_st : nullptr);
+        if (rc && attempt == 0) {        // leave both captures cleanly, then plain
+          cudaGraph_t junk;
+          cudaStreamCaptureStatus cs;
+          if (cudaStreamIsCapturing(s->body_st, &cs) == cudaSuccess &&
+              cs != cudaStreamCaptureStatusNone)
+            cudaStreamEndCapture(s->body_st, &junk);
+        }
+        cudaError_t e = cudaStreamEndCapture(st, &g);
+        if (rc == SP_OK && e == cudaSuccess &&
+            cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+          cudaGraphDestroy(g);
+          break;
+        }
+        if (g) cudaGraphDestroy(g);
+        ex = nullptr;
+        cudaGetLastError();
+        if (attempt == 1) {
+          if (rc) return rc;
+          return SP_ERR_CUDA;
+        }
+        s->use_cond = false;             // conditional capture unsupported here
+        rc = SP_OK;
+      }
       s->graphs[key] = ex;
       SP_CHECK(cudaGraphLaunch(ex, st));
     }

@@ -150,6 +150,7 @@ struct TcSmemTail {
   uint64_t empty[TC_STAGES];
   uint64_t done;
   uint32_t tmem_base;
+  int npre;                 // weight stages prefetched before the dependency wait
   int last;
   float inv_rms[128];
   float ssw[4][128];
@@ -187,12 +188,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
     // Weights do not depend on the previous kernel: start streaming the
-    // first stages before the programmatic dependency is resolved.
-    const uint64_t pw = policy_evict_first();
-    for (int i = 0; i < npre; ++i) {
-      mbar_expect_tx_only(&tail->full[i], TC_WTILE);
-      bulk_load(smem + i * STAGE, wtiles + (size_t)(c0 + i) * (TC_WTILE / 2), TC_WTILE,
-                &tail->full[i], pw);
+    // first stages before the programmatic dependency is resolved -- unless
+    // the run is already known to be skipped (a cancelled speculative run
+    // would otherwise still pull 64 KB per CTA of every GEMM of every layer).
+    // run_state only goes 0 -> 1 within a run and the run's gate kernel has
+    // completed before any of its GEMMs start, so a stale read can only be
+    // a 0 (a wasted prefetch), never a wrong skip.
+    const bool pre = !run_skipped(a.run_state);
+    tail->npre = pre ? npre : 0;
+    if (pre) {
+      const uint64_t pw = policy_evict_first();
+      for (int i = 0; i < npre; ++i) {
+        mbar_expect_tx_only(&tail->full[i], TC_WTILE);
+        bulk_load(smem + i * STAGE, wtiles + (size_t)(c0 + i) * (TC_WTILE / 2), TC_WTILE,
+                  &tail->full[i], pw);
+      }
     }
   }
   if (warp == 1) {
@@ -210,9 +220,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
   // kernel's outputs (activations, run_state, norm statistics)
   pdl_wait();
   pdl_trigger();
+  const int npre_done = tail->npre;
   if (run_skipped(a.run_state)) {        // consistent for the whole grid
     if (threadIdx.x == 0) {              // drain the weight prefetch
-      for (int i = 0; i < npre; ++i) {
+      for (int i = 0; i < npre_done; ++i) {
         mbar_arrive(&tail->full[i]);
         mbar_wait(&tail->full[i], 0);
       }
@@ -232,7 +243,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
       const int s = i % TC_STAGES;
       const uint32_t ph = (i / TC_STAGES) & 1;
       uint8_t* st = smem + s * STAGE;
-      if (i < npre) {                    // weights already in flight
+      if (i < npre_done) {               // weights already in flight
         mbar_expect_tx(&tail->full[s], XTILE);
       } else {
         mbar_wait(&tail->empty[s], ph ^ 1);
