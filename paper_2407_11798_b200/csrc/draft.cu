@@ -42,13 +42,17 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 }
 
 // Grid barrier over a counter zeroed before the launch (monotonic targets).
-__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target) {
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target,
+                                          unsigned a_spin_ns = 32) {
   __syncthreads();
   target += gridDim.x;
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     unsigned spins = 0;
+    // poll with a short back-off: 148 pollers on one L2 line otherwise
+    // queue behind each other at its slice (SP_DRAFT_SPIN_NS, default 32)
     while (ld_acquire_u32(bar) < target) {
+      __nanosleep(a_spin_ns);
       if (++spins > (1u << 28)) __trap();  // a lost CTA: fail loudly, never hang
     }
   }
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
           }
         }
       }
-      mark(1); grid_sync(a.bar, target); mark(9);
+      mark(1); grid_sync(a.bar, target, a.spin_ns); mark(9);
 
       // ------ B: attention over rows [0, row_m] + this head's O partial ------
       if (l + 1 < a.L) wload(0, l + 1);
@@ -711,7 +715,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
           __syncthreads();
         }
       }
-      mark(2); grid_sync(a.bar, target); mark(10);
+      mark(2); grid_sync(a.bar, target, a.spin_ns); mark(10);
 
       // --- D: x += sum_h O partials; h = silu(g) * u of rmsnorm(x) ----------
       for (int m = 0; m < n; ++m) {
@@ -778,7 +782,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
           }
         }
       }
-      mark(4); grid_sync(a.bar, target); mark(12);
+      mark(4); grid_sync(a.bar, target, a.spin_ns); mark(12);
 
       // ---------------- E: x = x_attn + h @ Wd (row owners) -----------------
       if (l + 1 < a.L) wload(1, l + 1);
@@ -822,7 +826,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
           }
         }
       }
-      mark(5); grid_sync(a.bar, target); mark(13);
+      mark(5); grid_sync(a.bar, target, a.spin_ns); mark(13);
     }
 
     // ---------------- H: final norm + LM head over the last token ----------
@@ -877,7 +881,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
         a.lm_part[blockIdx.x] = p;
       }
     }
-    mark(6); grid_sync(a.bar, target); mark(14);
+    mark(6); grid_sync(a.bar, target, a.spin_ns); mark(14);
     {
       // every CTA merges all partials in the same fixed order: thread t
       // takes partial t (one round trip), then butterflies and warps 0..7

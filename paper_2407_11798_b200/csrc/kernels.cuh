@@ -128,6 +128,7 @@ struct DraftArgs {
   int ring_stages, ring_bytes;  // cluster form: weight ring per CTA
   int nt;                       // cluster form: token rows of the activation buffers
   int use_mma;                  // cluster form: mma.sync GEMV for 16-row chunks
+  unsigned spin_ns;             // grid form: barrier poll back-off
 };
 
 size_t draft_smem_bytes(const DraftArgs& a);

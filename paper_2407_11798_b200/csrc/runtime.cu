@@ -1298,6 +1298,7 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
     if (!s->dprof) SP_CHECK(cudaMalloc((void**)&s->dprof, sizeof(long long) * 4096));
     a.prof = s->dprof;
   }
+  a.spin_ns = getenv("SP_DRAFT_SPIN_NS") ? (unsigned)atoi(getenv("SP_DRAFT_SPIN_NS")) : 32u;
   const char* kind = getenv("SP_DRAFT_KERNEL");
   if (kind && std::strcmp(kind, "grid") == 0) {
     if (s->draft_ctas <= 0) {

@@ -258,7 +258,7 @@ def worker_loop(model, lo, hi, rank, world, plane: ControlPlane, partitions,
         elif rtype == R_MARK:
             sr.stream.synchronize()
             if on_mark is not None:
-                on_mark(struct.unpack("<i", p[:4])[0])
+                on_mark(struct.unpack("<i", p[:4])[0], sr.stage.launches)
         elif rtype == R_SHUTDOWN:
             sr.stream.synchronize()
             while sr.works:
@@ -469,11 +469,13 @@ def bench_main(args):
     if rank != 0:
         lo, hi = ranges[rank - first]
         worker_loop(model, lo, hi, rank, world, plane, cfg.partitions, cfg.capacity,
-                    cfg.max_run_tokens, on_mark=lambda t: marks.append((t, time.perf_counter())),
+                    cfg.max_run_tokens, on_mark=lambda t, nl: marks.append((t, time.perf_counter(), nl)),
                     first=first)
         out = [None]
-        t = {m: v for m, v in marks}
-        dist.gather_object((t.get(1), t.get(2)), None, dst=0, group=gloo)
+        t = {m: v for m, v, _ in marks}
+        nl = {m: c for m, _, c in marks}
+        launched = (nl[2] - nl[1]) if (1 in nl and 2 in nl) else None
+        dist.gather_object((t.get(1), t.get(2), launched), None, dst=0, group=gloo)
         dist.barrier(group=gloo)
         plane.close()
         dist.destroy_process_group()
@@ -486,9 +488,13 @@ def bench_main(args):
     line = B.measure(eng, args, n_gpus=world, pipe=pipe)
     pipe.shutdown()
     times = [None] * world
-    dist.gather_object((None, None), times, dst=0, group=gloo)
-    spans = [t1 - t0 for (t0, t1) in times[1:] if t0 is not None and t1 is not None]
+    dist.gather_object((None, None, None), times, dst=0, group=gloo)
+    spans = [t1 - t0 for (t0, t1, _) in times[1:] if t0 is not None and t1 is not None]
     line["rank_spans_s"] = [round(x, 4) for x in spans]
+    # every rank's kernel launches in the timed region (rank 0's are in the line)
+    per = [line.get("gpu_launches")] + [c for (_, _, c) in times[1:]]
+    line["gpu_launches_per_rank"] = per
+    line["gpu_launches"] = sum(c for c in per if c)
     dist.barrier(group=gloo)
     plane.close(unlink=True)
     dist.destroy_process_group()
