@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
   constexpr int G = ATT_THREADS / LPR;    // rows in flight per pass
   static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "bad head dim");
   __shared__ float sc[ATT_CH];
+  extern __shared__ float mrg[];   // [nsplit][HD + 2] split partials (merging CTA)
   __shared__ float part[G][HD];
   __shared__ float red[ATT_THREADS / 32];
   __shared__ int last;
@@ -277,19 +278,31 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
     __syncthreads();
     if (!last) continue;  // (sc/part/red are rewritten only after a barrier)
     __threadfence();
+    // all partials of this (query, head) in one coalesced round trip, then
+    // the fixed split-order merge from shared memory
     const float* base = a.scratch + ((size_t)i * a.H + h) * a.nsplit * (HD + 2);
+    const float* src = base;
+    if (a.merge_smem) {   // (else the partials are read from L2 directly)
+      for (int idx = tid; idx < ns * (HD + 2); idx += ATT_THREADS) mrg[idx] = __ldcg(base + idx);
+      __syncthreads();
+      src = mrg;
+    }
     float M = -INFINITY;
-    for (int ss = 0; ss < ns; ++ss) M = fmaxf(M, ld_volatile_f(base + ss * (HD + 2)));
+    for (int ss = 0; ss < ns; ++ss)
+      M = fmaxf(M, a.merge_smem ? src[ss * (HD + 2)] : __ldcg(src + ss * (HD + 2)));
     float L = 0.f;
     for (int ss = 0; ss < ns; ++ss) {
-      const float* b = base + ss * (HD + 2);
-      L += ld_volatile_f(b + 1) * __expf(ld_volatile_f(b) - M);
+      const float* b = src + ss * (HD + 2);
+      const float m0 = a.merge_smem ? b[0] : __ldcg(b), l0 = a.merge_smem ? b[1] : __ldcg(b + 1);
+      L += l0 * __expf(m0 - M);
     }
     for (int d = tid; d < HD; d += ATT_THREADS) {
       float o = 0.f;
       for (int ss = 0; ss < ns; ++ss) {
-        const float* b = base + ss * (HD + 2);
-        o += ld_volatile_f(b + 2 + d) * __expf(ld_volatile_f(b) - M);
+        const float* b = src + ss * (HD + 2);
+        const float m0 = a.merge_smem ? b[0] : __ldcg(b);
+        const float ov = a.merge_smem ? b[2 + d] : __ldcg(b + 2 + d);
+        o += ov * __expf(m0 - M);
       }
       store(d, o / L);
     }
@@ -298,17 +311,161 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
   }
 }
 
+
+// Decode/verify attention without splits: one CTA per (head, query). The
+// query's plan is staged in shared memory (one coalesced round trip); each
+// row group walks plan entries g, g+G, ... with K and V of the next PF rows
+// in flight while the current ones are folded into a per-group online
+// softmax (running max, sum, accumulator); the G group states merge in
+// group order at the end.  No partials, tickets or second pass: the launch
+// is one load-latency chain long.  Order is fixed per query (batch
+// invariant).
+template <typename T, int HD>
+__global__ void __launch_bounds__(ATT_THREADS) attn_flat_kernel(const AttnArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int LPR = HD / VEC;
+  constexpr int G = ATT_THREADS / LPR;
+  constexpr int PF = 4;
+  extern __shared__ int32_t splan[];          // [len]
+  __shared__ float gm[G], gl[G];
+  __shared__ float gacc[G][HD];
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 &&
+      a.cancel_word != nullptr && a.run_state_w != nullptr) {
+    if (ld_volatile(a.cancel_word) == a.run_id) atomicExch(a.run_state_w, 1);
+  }
+  if (run_skipped(a.run_state)) return;
+  const int h = blockIdx.x, i = blockIdx.y;
+  const int len = a.vis_len[i];
+  const int kh = h / (a.H / a.KH);
+  const int kvd = a.KH * HD;
+  const int tid = threadIdx.x, g = tid / LPR, l = tid % LPR;
+  const int32_t* plan = a.vis + (size_t)i * a.ld_vis;
+  for (int e = tid; e < len; e += ATT_THREADS) splan[e] = plan[e];
+  float qv[VEC];
+  {
+    const float* qp = a.q + (size_t)i * a.H * HD + h * HD + l * VEC;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) qv[j] = qp[j] * a.scale;
+  }
+  __syncthreads();
+  const T* Kc = reinterpret_cast<const T*>(a.k) + kh * HD + l * VEC;
+  const T* Vc = reinterpret_cast<const T*>(a.v) + kh * HD + l * VEC;
+  float m = -INFINITY, lsum = 0.f, acc[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
+  uint4 kb[2][PF], vb[2][PF];
+  auto load = [&](int buf, int e0) {
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+      const int e = e0 + p * G;
+      const int row = e < len ? splan[e] : splan[0];
+      kb[buf][p] = ld_stream16(Kc + (size_t)row * kvd);
+      vb[buf][p] = ld_stream16(Vc + (size_t)row * kvd);
+    }
+  };
+  int cur = 0;
+  load(0, g);
+  // the trip count is the same for every group (shuffles need whole warps)
+  for (int base = 0; base < len; base += G * PF) {
+    const int e0 = base + g;
+    if (base + G * PF < len) load(cur ^ 1, e0 + G * PF);   // next rows in flight
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+      const int e = e0 + p * G;
+      float kf[VEC];
+      VecTraits<T>::unpack(kb[cur][p], kf);
+      float d = 0.f;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) d = __fmaf_rn(qv[j], kf[j], d);
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      if (e < len) {
+        float vf[VEC];
+        VecTraits<T>::unpack(vb[cur][p], vf);
+        if (d > m) {
+          const float c = __expf(m - d);
+          lsum = __fmul_rn(lsum, c);
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) acc[j] = __fmul_rn(acc[j], c);
+          m = d;
+        }
+        const float pr = __expf(d - m);
+        lsum = __fadd_rn(lsum, pr);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[j] = __fmaf_rn(pr, vf[j], acc[j]);
+      }
+    }
+    cur ^= 1;
+  }
+  if (l == 0) { gm[g] = m; gl[g] = lsum; }
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) gacc[g][l * VEC + j] = acc[j];
+  __syncthreads();
+  const size_t obase = (size_t)i * a.H * HD + h * HD;
+  for (int dd = tid; dd < HD; dd += ATT_THREADS) {
+    float M = -INFINITY;
+    for (int q = 0; q < G; ++q) M = fmaxf(M, gm[q]);
+    float L = 0.f, o = 0.f;
+    for (int q = 0; q < G; ++q) {
+      if (gm[q] == -INFINITY) continue;
+      const float c = __expf(gm[q] - M);
+      L = __fadd_rn(L, __fmul_rn(gl[q], c));
+      o = __fadd_rn(o, __fmul_rn(gacc[q][dd], c));
+    }
+    const float v = o / L;
+    if (a.out_bf16) reinterpret_cast<__nv_bfloat16*>(a.out)[obase + dd] = __float2bfloat16_rn(v);
+    else a.out[obase + dd] = v;
+  }
+}
+
+template <typename T, int HD>
+static cudaError_t launch_attn_flat(AttnArgs a, cudaStream_t st) {
+  const size_t smem = sizeof(int32_t) * (size_t)a.ld_vis;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    static size_t configured = 0;
+    if (configured < smem) {
+      cudaFuncSetAttribute(attn_flat_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      configured = smem;
+    }
+  }
+  return launch_pdl(attn_flat_kernel<T, HD>, dim3(a.H, a.n), dim3(ATT_THREADS), smem, st, a);
+}
+
+template <typename T, int HD>
+static cudaError_t launch_attn_hd(dim3 grid, AttnArgs a, cudaStream_t st) {
+  // the unsplit variant is kept for experiments (SP_ATTN_FLAT=1): on the 7B
+  // decode it is no faster than 32-entry splits (one CTA per head keeps too
+  // few bytes in flight)
+  static const bool flat = getenv("SP_ATTN_FLAT") != nullptr;
+  if (flat && (size_t)a.ld_vis * 4 <= 200 * 1024) return launch_attn_flat<T, HD>(a, st);
+  const size_t smem = sizeof(float) * (size_t)a.nsplit * (HD + 2);
+  a.merge_smem = smem <= 96 * 1024 ? 1 : 0;
+  if (a.merge_smem && smem > 48 * 1024) {
+    static size_t configured = 0;
+    if (configured < smem) {
+      cudaFuncSetAttribute(attn_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           96 * 1024);
+      configured = 96 * 1024;
+    }
+  }
+  return launch_pdl(attn_kernel<T, HD>, grid, dim3(ATT_THREADS), a.merge_smem ? smem : 0, st, a);
+}
+
 template <typename T>
 static cudaError_t attn_dispatch(const AttnArgs& a, int hd, cudaStream_t st) {
   // about 4 CTAs per SM in total; splits beyond gridDim.z loop in-CTA
   const int want = (4 * 148 + a.H * a.n - 1) / (a.H * a.n);
   const dim3 grid(a.H, a.n, max(1, min(a.nsplit, want)));
   switch (hd) {
-    case 8: return launch_pdl(attn_kernel<T, 8>, grid, dim3(ATT_THREADS), 0, st, a);
-    case 16: return launch_pdl(attn_kernel<T, 16>, grid, dim3(ATT_THREADS), 0, st, a);
-    case 32: return launch_pdl(attn_kernel<T, 32>, grid, dim3(ATT_THREADS), 0, st, a);
-    case 64: return launch_pdl(attn_kernel<T, 64>, grid, dim3(ATT_THREADS), 0, st, a);
-    case 128: return launch_pdl(attn_kernel<T, 128>, grid, dim3(ATT_THREADS), 0, st, a);
+    case 8: return launch_attn_hd<T, 8>(grid, a, st);
+    case 16: return launch_attn_hd<T, 16>(grid, a, st);
+    case 32: return launch_attn_hd<T, 32>(grid, a, st);
+    case 64: return launch_attn_hd<T, 64>(grid, a, st);
+    case 128: return launch_attn_hd<T, 128>(grid, a, st);
     default: return cudaErrorInvalidValue;
   }
 }

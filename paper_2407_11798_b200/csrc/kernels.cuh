@@ -42,6 +42,7 @@ struct AttnArgs {
   int run_id;
   int* err;
   int out_bf16;            // write the output as bf16 (tensor-core path input)
+  int merge_smem;   // set by the launcher: merge partials through shared memory
 };
 
 struct LmPartial {

@@ -145,9 +145,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-struct TcSmemTail {
-  uint64_t full[TC_STAGES];
-  uint64_t empty[TC_STAGES];
+template <int ST>
+struct TcSmemTailT {
+  uint64_t full[ST];
+  uint64_t empty[ST];
   uint64_t done;
   uint32_t tmem_base;
   int npre;                 // weight stages prefetched before the dependency wait
@@ -157,7 +158,10 @@ struct TcSmemTail {
 };
 
 // ---- the kernel -------------------------------------------------------------
-template <int NT, int EPI, bool NORM>
+// ST = ring depth: 4 stages (2 CTAs/SM) for wide grids, 10 (one CTA/SM,
+// 160 KB of weights in flight) when the grid fits one CTA per SM -- a decode
+// GEMM is bounded by the bytes each SM keeps in flight
+template <int NT, int EPI, bool NORM, int ST>
 __global__ void __launch_bounds__(TC_THREADS)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
   constexpr int XTILE = NT * TC_BK * 2;
@@ -166,7 +170,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
-  TcSmemTail* tail = reinterpret_cast<TcSmemTail*>(smem + TC_STAGES * STAGE);
+  TcSmemTailT<ST>* tail = reinterpret_cast<TcSmemTailT<ST>*>(smem + ST * STAGE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, split = blockIdx.y, nsplit = gridDim.y;
@@ -174,13 +178,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
   const int c0 = (int)((long)nchunk * split / nsplit);
   const int c1 = (int)((long)nchunk * (split + 1) / nsplit);
   const int nloc = c1 - c0;
-  const int npre = nloc < TC_STAGES ? nloc : TC_STAGES;
+  const int npre = nloc < ST ? nloc : ST;
   // this CTA's weight tiles [tile][c0..c1) are one contiguous run
   const __nv_bfloat16* wtiles =
       reinterpret_cast<const __nv_bfloat16*>(a.w) + (size_t)tile * nchunk * (TC_WTILE / 2);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < ST; ++s) {
       mbar_init(&tail->full[s], 1);
       mbar_init(&tail->empty[s], 1);
     }
@@ -240,8 +244,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
     // ---- TMA producer ----
     const uint64_t pw = policy_evict_first(), px = policy_evict_last();
     for (int i = 0; i < nloc; ++i) {
-      const int s = i % TC_STAGES;
-      const uint32_t ph = (i / TC_STAGES) & 1;
+      const int s = i % ST;
+      const uint32_t ph = (i / ST) & 1;
       uint8_t* st = smem + s * STAGE;
       if (i < npre_done) {               // weights already in flight
         mbar_expect_tx(&tail->full[s], XTILE);
@@ -256,8 +260,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
     // ---- MMA issuer ----
     constexpr uint32_t IDESC = idesc_bf16(TC_BM, NT);
     for (int i = 0; i < nloc; ++i) {
-      const int s = i % TC_STAGES;
-      const uint32_t ph = (i / TC_STAGES) & 1;
+      const int s = i % ST;
+      const uint32_t ph = (i / ST) & 1;
       mbar_wait(&tail->full[s], ph);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE);
@@ -459,14 +463,14 @@ bool make_map_bf16(CUtensorMap* map, const void* base, long rows, long cols, lon
          CUDA_SUCCESS;
 }
 
-template <int NT, int EPI, bool NORM>
+template <int NT, int EPI, bool NORM, int ST>
 static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
                              cudaStream_t st) {
   constexpr int STAGE = TC_WTILE + NT * TC_BK * 2;
-  const int smem = TC_STAGES * STAGE + (int)sizeof(TcSmemTail) + 1024;
+  const int smem = ST * STAGE + (int)sizeof(TcSmemTailT<ST>) + 1024;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(tc_gemm_kernel<NT, EPI, NORM>,
+    cudaFuncSetAttribute(tc_gemm_kernel<NT, EPI, NORM, ST>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
@@ -485,24 +489,24 @@ static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<NT, EPI, NORM>, x, a);
+  return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<NT, EPI, NORM, ST>, x, a);
 }
 
-template <int NT>
+template <int NT, int ST>
 static cudaError_t launch_epi(const CUtensorMap& x, const TcArgs& a, int ksplit,
                               cudaStream_t st) {
   switch (a.epi) {
     case SP_EPI_QKV:
-      return a.norm ? launch_nt<NT, SP_EPI_QKV, true>(x, a, ksplit, st)
-                    : launch_nt<NT, SP_EPI_QKV, false>(x, a, ksplit, st);
+      return a.norm ? launch_nt<NT, SP_EPI_QKV, true, ST>(x, a, ksplit, st)
+                    : launch_nt<NT, SP_EPI_QKV, false, ST>(x, a, ksplit, st);
     case SP_EPI_SWIGLU:
-      return a.norm ? launch_nt<NT, SP_EPI_SWIGLU, true>(x, a, ksplit, st)
-                    : launch_nt<NT, SP_EPI_SWIGLU, false>(x, a, ksplit, st);
+      return a.norm ? launch_nt<NT, SP_EPI_SWIGLU, true, ST>(x, a, ksplit, st)
+                    : launch_nt<NT, SP_EPI_SWIGLU, false, ST>(x, a, ksplit, st);
     case SP_EPI_RESID:
-      return launch_nt<NT, SP_EPI_RESID, false>(x, a, ksplit, st);
+      return launch_nt<NT, SP_EPI_RESID, false, ST>(x, a, ksplit, st);
     case SP_EPI_STORE:
-      return a.norm ? launch_nt<NT, SP_EPI_STORE, true>(x, a, ksplit, st)
-                    : launch_nt<NT, SP_EPI_STORE, false>(x, a, ksplit, st);
+      return a.norm ? launch_nt<NT, SP_EPI_STORE, true, ST>(x, a, ksplit, st)
+                    : launch_nt<NT, SP_EPI_STORE, false, ST>(x, a, ksplit, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -527,13 +531,33 @@ int tc_ksplit(int n_rows, int k, int target_ctas) {
 // maps[1] the NT=128 one.
 cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st) {
   const int nt = tc_nt_for(a.m);
-  const int budget = a.max_ctas > 0 ? a.max_ctas : 2 * 148;
-  int ksplit = a.ksplit > 0 ? a.ksplit : tc_ksplit(a.n_rows, a.k, budget);
+  const int budget = a.max_ctas > 0 ? a.max_ctas : 296;   // at 2 CTAs per SM
+  const int sms = budget / 2;                              // at 1 CTA per SM
+  const int tiles = a.n_rows / TC_BM, nchunk = a.k / TC_BK;
+  int ksplit;
+  bool deep = false;
+  // deep when the tile count leaves room to split at least 2-way within one
+  // CTA per SM (measured on the 7B shapes: O 10.9 -> 10.4 us, down 18.7 ->
+  // 17.4; QKV (96 tiles) stays faster at 2 shallow CTAs per SM)
+  if (nt == 16 && getenv("SP_TC_SHALLOW") == nullptr &&
+      (a.ksplit > 0 ? tiles * a.ksplit <= sms : 2 * tiles <= sms)) {
+    // one CTA per SM with a deep ring: split so the grid still fits one wave
+    ksplit = a.ksplit > 0 ? a.ksplit
+                          : max(1, min(min(sms / tiles, nchunk / 16), 8));
+    while (ksplit & (ksplit - 1)) ksplit &= ksplit - 1;
+    deep = true;
+  } else {
+    ksplit = a.ksplit > 0 ? a.ksplit : tc_ksplit(a.n_rows, a.k, budget);
+  }
   if (ksplit > 8) ksplit = 8;
   for (int t0 = 0; t0 < a.m; t0 += nt) {
     a.tok0 = t0;
-    cudaError_t e = nt == 16 ? launch_epi<16>(xmaps[0], a, ksplit, st)
-                             : launch_epi<128>(xmaps[1], a, ksplit, st);
+    cudaError_t e;
+    if (nt == 16)
+      e = deep ? launch_epi<16, 10>(xmaps[0], a, ksplit, st)
+               : launch_epi<16, 4>(xmaps[0], a, ksplit, st);
+    else
+      e = launch_epi<128, 4>(xmaps[1], a, ksplit, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -1,0 +1,50 @@
+"""Kernel timeline of ONE graph-replayed 7B decode stage-run (32 layers + LM
+head, 1 token): per kernel kind, the increment it adds to the run's critical
+path (end-to-end of consecutive kernel ends, robust to PDL overlap)."""
+import collections
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2407_11798_b200 as sp
+from paper_2407_11798_b200.model import BatchToken, encode_tokens
+from paper_2407_11798_b200.pipeline import LocalPipeline
+
+cfg = sp.llama_config("llama2-7b")
+m = sp.build_model(cfg, torch.device("cuda", 0))
+pipe = LocalPipeline(m, [(0, 32)], partitions=8, capacity=4096, max_tokens=256)
+ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 384
+pre = [BatchToken(5 + (i % 100), i, frozenset([0]), i == ctx - 1) for i in range(ctx)]
+for c0 in range(0, ctx, 128):
+    chunk = pre[c0:c0 + 128]
+    pipe.launch(c0, 0, encode_tokens(chunk), 0, [len(chunk) - 1])
+    pipe.wait()
+rid = 1000
+for rep in range(4):   # warm + capture the graph
+    pipe.launch(rid, 1, encode_tokens([BatchToken(7, ctx + rep, frozenset([0]), True)]), 0, [0])
+    pipe.wait()
+    rid += 1
+torch.cuda.synchronize()
+with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+    pipe.launch(rid, 1, encode_tokens([BatchToken(7, ctx + 4, frozenset([0]), True)]), 0, [0])
+    pipe.wait()
+    torch.cuda.synchronize()
+prof.export_chrome_trace("/tmp/st.json")
+ev = [e for e in json.load(open("/tmp/st.json"))["traceEvents"] if e.get("cat") == "kernel"]
+ev.sort(key=lambda e: e["ts"] + e["dur"])
+t_start = min(e["ts"] for e in ev)
+prev_end = t_start
+inc = collections.defaultdict(lambda: [0, 0.0])
+for e in ev:
+    end = e["ts"] + e["dur"]
+    k = e["name"].split("(")[0].replace("void ", "").replace("sp::", "")[:44]
+    inc[k][0] += 1
+    inc[k][1] += max(0.0, end - prev_end)
+    prev_end = max(prev_end, end)
+total = prev_end - t_start
+print(f"ctx {ctx}: {len(ev)} kernels, run span {total:.1f} us")
+for k, (n, t) in sorted(inc.items(), key=lambda x: -x[1][1]):
+    print(f"  {k:44s} n={n:3d}  critical-path {t:8.1f} us  ({t / n:6.2f}/launch)")
