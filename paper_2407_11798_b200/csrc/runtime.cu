@@ -155,12 +155,19 @@ __global__ void prep_kernel(const float* __restrict__ x, int d,
 // folds the device-visible cancel word into run_state; kernels launched
 // after it skip.  A dedicated launch keeps every multi-CTA kernel's view of
 // run_state consistent (no mid-kernel flips).
-__global__ void observe_kernel(const RunHdr* hdr, const int* cancel_table, int* run_state) {
+__global__ void observe_kernel(const RunHdr* hdr, const int* cancel_table, int* run_state,
+                               unsigned long long cond) {
   pdl_wait();
   pdl_trigger();
-  if (!(hdr->flags & SP_FWD_SKIPPABLE) || hdr->kind != SP_KIND_SPEC || hdr->cancel_idx < 0)
-    return;
-  if (ld_volatile(cancel_table + hdr->cancel_idx) == hdr->run_id) *run_state = 1;
+  int skip = ld_volatile(run_state);
+  if ((hdr->flags & SP_FWD_SKIPPABLE) && hdr->kind == SP_KIND_SPEC && hdr->cancel_idx >= 0 &&
+      ld_volatile(cancel_table + hdr->cancel_idx) == hdr->run_id) {
+    *run_state = 1;
+    skip = 1;
+  }
+  // graph-replayed runs: the next block of layers sits in its own
+  // conditional node -- a run cancelled mid-flight skips the rest outright
+  if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, skip ? 0u : 1u);
 }
 
 __global__ void chain_begin_kernel(const int* tip, int* gate, float cutoff,
@@ -198,7 +205,16 @@ struct LayerW {
 
 static constexpr int TC_SCRATCH_FLOATS = 8 << 20;
 static constexpr int TC_TICKETS = 4096;
-static constexpr int OBSERVE_EVERY = 4;  // layers between cancel observations
+// layers between cancel observations / per conditional graph node (each
+// IF node costs a few us on a full run: it breaks the PDL chain)
+static int observe_every() {
+  static const int v = getenv("SP_OBSERVE_EVERY") ? atoi(getenv("SP_OBSERVE_EVERY")) : 4;
+  return v > 0 ? v : 1;
+}
+static int cond_block() {
+  static const int v = getenv("SP_COND_BLOCK") ? atoi(getenv("SP_COND_BLOCK")) : 8;
+  return v > 0 ? v : 1;
+}
 
 static constexpr int DESC_RING = 64;
 
@@ -720,9 +736,38 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     // early inference cancellation: observe the cancel word between layers
     // (engine.py:602-612 drains cancels between layers); a no-op for runs
     // that are not cancellable (read from the header)
-    if (s->cancel_table && l + 1 < layer_b && ((l + 1 - layer_a) % OBSERVE_EVERY) == 0)
+    if (s->cancel_table && l + 1 < layer_b && ((l + 1 - layer_a) % observe_every()) == 0) {
+      const bool block_edge = body_st && ((l + 1 - layer_a) % cond_block()) == 0;
+      unsigned long long next = 0;
+      if (block_edge) {   // handle of the next block's IF node (resets to 0 per launch)
+        cudaGraphConditionalHandle h;
+        SP_CHECK(cudaGraphConditionalHandleCreate(&h, cap_graph, 0,
+                                                  cudaGraphCondAssignDefault));
+        next = (unsigned long long)h;
+      }
       SP_CHECK(launch_pdl(observe_kernel, dim3(1), dim3(1), 0, st, (const RunHdr*)s->hdr,
-                          s->cancel_table, s->run_state));
+                          s->cancel_table, s->run_state, next));
+      if (block_edge) {
+        // close this block's body, chain the next IF node in the outer graph
+        cudaGraph_t g;
+        SP_CHECK(cudaStreamEndCapture(body_st, &g));
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        SP_CHECK(cudaStreamGetCaptureInfo(outer, &cs, nullptr, nullptr, &deps, &nd));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = (cudaGraphConditionalHandle)next;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cn;
+        SP_CHECK(cudaGraphAddNode(&cn, cap_graph, deps, nd, &cp));
+        SP_CHECK(cudaStreamUpdateCaptureDependencies(outer, &cn, 1,
+                                                     cudaStreamSetCaptureDependencies));
+        SP_CHECK(cudaStreamBeginCaptureToGraph(body_st, cp.conditional.phGraph_out[0], nullptr,
+                                               nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      }
+    }
   }
   if (body_st) {
     cudaGraph_t g;

@@ -22,10 +22,11 @@ pipe.wait()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 SPEC = _lib.SP_KIND_SPEC
 flags = _lib.SP_FWD_SKIPPABLE
-times = {"run": [], "skipped": []}
+import time
+times = {"run": [], "skipped": [], "cancelled_at_1ms": []}
 rid = 2
 for rep in range(12):
-    for kind in ("run", "skipped"):
+    for kind in ("run", "skipped", "cancelled_at_1ms"):
         toks = encode_tokens([BatchToken(7, 128 + rep, frozenset([1]), True)])
         if kind == "skipped":
             pipe.cancel_run(rid)
@@ -33,6 +34,9 @@ for rep in range(12):
         ev[0].record(pipe.stream)
         pipe.launch(rid, SPEC, toks, flags, [0])
         ev[1].record(pipe.stream)
+        if kind == "cancelled_at_1ms":   # mid-flight: the head cancels ~1 ms in
+            time.sleep(0.001)
+            pipe.cancel_run(rid)
         pipe.wait()
         ev[1].synchronize()
         if rep >= 2:
