@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
   __shared__ float inv_s[HD / 2];
   __shared__ float part[DR_THREADS / (HD / 8)][HD];
   __shared__ float attn_s[HD];
+  __shared__ float gstat[DR_THREADS / (HD / 8)][2];
   __shared__ float wred[DR_WARPS];
   __shared__ int last;
   __shared__ float lm_w[DR_WARPS][4];
@@ -551,6 +552,120 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
       if (l + 1 < a.L) wload(0, l + 1);
       else if (k < steps) wload(0, 0);
       head_prefetch(l);
+      if (n == 1 && (int)gridDim.x >= 2 * a.H) {
+        // single token: head groups of GS CTAs; every CTA of a group runs the
+        // head's whole attention (redundantly, K/V stream from L2) and then
+        // its own d/GS rows of the head's W_o columns -- no split merge, no
+        // idle CTAs
+        constexpr int LPR = HD / 8;
+        constexpr int RPP = DR_THREADS / LPR;    // row groups (rows per pass)
+        constexpr int PASSES = 8;                // rows in flight per chunk: RPP*8
+        const int GS = (int)gridDim.x / a.H;
+        const int hh = blockIdx.x / GS, jm = blockIdx.x % GS;
+        if (hh < a.H) {
+          const int grp = tid / LPR, li = tid % LPR;
+          const int kh = hh / (a.H / a.KH);
+          const int len = rowA + 1;
+          float qv[8];
+          {
+            const float* qp = a.q + hh * HD + li * 8;
+            const float4 q0 = __ldcg(reinterpret_cast<const float4*>(qp));
+            const float4 q1 = __ldcg(reinterpret_cast<const float4*>(qp + 4));
+            qv[0] = q0.x * att_scale; qv[1] = q0.y * att_scale;
+            qv[2] = q0.z * att_scale; qv[3] = q0.w * att_scale;
+            qv[4] = q1.x * att_scale; qv[5] = q1.y * att_scale;
+            qv[6] = q1.z * att_scale; qv[7] = q1.w * att_scale;
+          }
+          // per row-group online softmax over rows grp, grp+RPP, ... (fixed order)
+          float mx = -INFINITY, ls = 0.f, acc[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) acc[t] = 0.f;
+          for (int c0 = 0; c0 < len; c0 += RPP * PASSES) {
+            uint4 kr[PASSES], vr[PASSES];
+#pragma unroll
+            for (int p = 0; p < PASSES; ++p) {
+              const int r = c0 + p * RPP + grp;
+              const size_t off = (size_t)r * kvd + kh * HD + li * 8;
+              kr[p] = r < len ? ldcg16(Kc + off) : make_uint4(0, 0, 0, 0);
+              vr[p] = r < len ? ldcg16(Vc + off) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int p = 0; p < PASSES; ++p) {
+              const int r = c0 + p * RPP + grp;
+              float kf[8];
+              bf16x8_to_f32(kr[p], kf);
+              float sdot = 0.f;
+#pragma unroll
+              for (int t = 0; t < 8; ++t) sdot = __fmaf_rn(qv[t], kf[t], sdot);
+#pragma unroll
+              for (int o = LPR / 2; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+              if (r < len) {
+                float vf[8];
+                bf16x8_to_f32(vr[p], vf);
+                if (sdot > mx) {
+                  const float cc = __expf(mx - sdot);
+                  ls = __fmul_rn(ls, cc);
+#pragma unroll
+                  for (int t = 0; t < 8; ++t) acc[t] = __fmul_rn(acc[t], cc);
+                  mx = sdot;
+                }
+                const float pr = __expf(sdot - mx);
+                ls = __fadd_rn(ls, pr);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) acc[t] = __fmaf_rn(pr, vf[t], acc[t]);
+              }
+            }
+          }
+          // row groups -> head output in group order (shared memory)
+          if (li == 0) { gstat[grp][0] = mx; gstat[grp][1] = ls; }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) part[grp][li * 8 + t] = acc[t];
+          __syncthreads();
+          for (int e = tid; e < HD; e += DR_THREADS) {
+            float M = -INFINITY;
+            for (int q = 0; q < RPP; ++q) M = fmaxf(M, gstat[q][0]);
+            float L = 0.f, o = 0.f;
+            for (int q = 0; q < RPP; ++q) {
+              if (gstat[q][0] == -INFINITY) continue;
+              const float cc = __expf(gstat[q][0] - M);
+              L = __fadd_rn(L, __fmul_rn(gstat[q][1], cc));
+              o = __fadd_rn(o, __fmul_rn(part[q][e], cc));
+            }
+            attn_s[e] = o / L;
+          }
+          __syncthreads();
+          // this member's rows of the head's O columns (SWZ8 units)
+          const int r0 = (int)(((long)d * jm) / GS), r1 = (int)(((long)d * (jm + 1)) / GS);
+          constexpr int LR = HD / 8, RW = 32 / LR;
+          const int lr = lane % LR, rw = lane / LR;
+          float av[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) av[j] = attn_s[lr * 8 + j];
+          float* op = a.opart + (size_t)hh * d;
+          for (int rb = r0 + warp * RW; rb < r1; rb += DR_WARPS * RW * 4) {
+            uint4 wv[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int r = rb + b * DR_WARPS * RW + rw;
+              const int un = (hh * HD) / 8 + lr;
+              wv[b] = r < r1 ? ld_stream16(Lw.o + (size_t)r * qd + (size_t)(un ^ (r & 7)) * 8)
+                             : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              float wf[8];
+              bf16x8_to_f32(wv[b], wf);
+              float t = 0.f;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) t = __fmaf_rn(wf[j], av[j], t);
+#pragma unroll
+              for (int o = LR / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+              const int r = rb + b * DR_WARPS * RW + rw;
+              if (lr == 0 && r < r1) op[r] = t;
+            }
+          }
+        }
+      } else
       {
         // one CTA per (token, head, split of ACH rows); each thread issues
         // ALL of its K and V loads up front (one round trip)
