@@ -520,7 +520,11 @@ __global__ void __launch_bounds__(K2_THREADS, 1) draft_cluster_kernel(const Draf
       const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(
           ring + (size_t)st * a.ring_bytes) + (size_t)r_lo * ldw;
       float res[NT];
-      if (cnt > 0) {
+      if (cnt > 0 && a.diag_nocompute) {   // diagnostics: streaming/sync cost only
+#pragma unroll
+        for (int m = 0; m < NT; ++m) res[m] = 0.f;
+        epi(crow + r_lo, false, res, R);
+      } else if (cnt > 0) {
         const int rg = sg.row0g + crow + r_lo;
         if (R == 8) k2_rows<8, NT>(W, ldw, cnt, K, xs, ldx, n, res, rg);
         else if (R == 4) k2_rows<4, NT>(W, ldw, cnt, K, xs, ldx, n, res, rg);

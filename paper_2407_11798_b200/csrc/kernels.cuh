@@ -130,6 +130,7 @@ struct DraftArgs {
   int nt;                       // cluster form: token rows of the activation buffers
   int use_mma;                  // cluster form: mma.sync GEMV for 16-row chunks
   unsigned spin_ns;             // grid form: barrier poll back-off
+  int diag_nocompute;           // cluster form, diagnostics only: skip the GEMV math
 };
 
 size_t draft_smem_bytes(const DraftArgs& a);

@@ -1389,6 +1389,7 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
     if (a.ring_stages > 16) a.ring_stages = 16;
     a.nt = nt;
     a.use_mma = getenv("SP_DRAFT_MMA") && atoi(getenv("SP_DRAFT_MMA")) == 1;
+    a.diag_nocompute = getenv("SP_DRAFT_DIAG_NOCOMPUTE") != nullptr;
     SP_CHECK(launch_draft_cluster(a, s->draft_cluster, st));
   }
   s->n_cells += total;
