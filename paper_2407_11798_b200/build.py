@@ -24,6 +24,8 @@ OBJ = os.path.join(HERE, "csrc", "_obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
            "-Xcompiler", "-fPIC", "-Xptxas", "-O3", "-I", INCLUDE]
+# experiments only (e.g. SP_NVCC_EXTRA="-DSP_ATT_CH=64")
+NVFLAGS += os.environ.get("SP_NVCC_EXTRA", "").split()
 
 
 def _nvcc() -> str:

@@ -116,7 +116,10 @@ plan_kernel(const int32_t* __restrict__ cell_pos,
 // fixed order (last-arriving CTA), so results do not depend on scheduling.
 // ---------------------------------------------------------------------------
 constexpr int ATT_THREADS = 128;
-constexpr int ATT_CH = 32;   // plan entries per split: one load pass, K and V together
+#ifndef SP_ATT_CH
+#define SP_ATT_CH 32
+#endif
+constexpr int ATT_CH = SP_ATT_CH;   // plan entries per split: one load pass, K and V together
 constexpr int ATT_UNROLL = 4;
 
 

@@ -40,7 +40,10 @@ prev_end = t_start
 inc = collections.defaultdict(lambda: [0, 0.0])
 for e in ev:
     end = e["ts"] + e["dur"]
-    k = e["name"].split("(")[0].replace("void ", "").replace("sp::", "")[:44]
+    k = e["name"].split("(")[0].replace("void ", "").replace("sp::", "")[:36]
+    g = e.get("args", {}).get("grid")
+    if g and "gemm" in k:
+        k += " g" + "x".join(str(v) for v in g)
     inc[k][0] += 1
     inc[k][1] += max(0.0, end - prev_end)
     prev_end = max(prev_end, end)
