@@ -231,6 +231,10 @@ def bench_knobs(args) -> dict:
         v = getattr(args, k, None)
         if v is not None:
             kw[k] = v
+    if getattr(args, "no_ramp", False):
+        kw["spec_ramp"] = False
+    if getattr(args, "free_draft", False):   # experiment only: draft proposals cost nothing
+        kw["draft_charge"] = False
     return kw
 
 
@@ -318,7 +322,9 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
                    "engine": {"microbatch": eng.cfg.microbatch, "partitions": eng.cfg.partitions,
                               "cutoff": eng.cfg.cutoff, "draft_kernel":
                               os.environ.get("SP_DRAFT_KERNEL", "cluster")
-                              if os.environ.get("SP_DRAFT_FUSED", "1") != "0" else "per-forward"},
+                              if os.environ.get("SP_DRAFT_FUSED", "1") != "0" else "per-forward",
+                              "spec_ramp": eng.cfg.spec_ramp,
+                              **({"free_draft": True} if not eng.cfg.draft_charge else {})},
                    "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
         "itl_ms": round(itl * 1e3, 3),
         "acceptance_rate": round(statistics.mean(r.metrics.acceptance_rate for r in res), 4),
@@ -378,6 +384,10 @@ def main():
     ap.add_argument("--gen-len", type=int, default=GEN_LEN)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ramp", action="store_true",
+                    help="engine knob: full micro-batches from a fresh chain (spec_ramp=False)")
+    ap.add_argument("--free-draft", action="store_true",
+                    help="experiment only (not a headline): the synthetic draft skips its forward")
     ap.add_argument("--microbatch", type=int, default=None)
     ap.add_argument("--partitions", type=int, default=None)
     ap.add_argument("--cutoff", type=float, default=None)

@@ -100,6 +100,11 @@ class ExperimentConfig:
                                          # lower-latency CUDA-core GEMV path
     draft_sm_reserve: int = 16           # SMs kept free of target GEMMs on the
                                          # draft's GPU (so draft kernels start at once)
+    spec_ramp: bool = True               # reference: the continuous micro-batch cap
+                                         # ramps with the unverified chain depth
+                                         # (engine.py:1027-1030); False asks for
+                                         # `microbatch` tokens every time (a GPU
+                                         # stage-run costs the same for 1..16 tokens)
 
     def validate(self) -> None:
         if self.mode not in MODES:
@@ -639,7 +644,9 @@ class Head:
         ctx = self.accepted + [t for _, t in self.pending]
         cp = self._common_prefix(self.mirror, ctx)
         if self.cfg.continuous:
-            cap = min(self.cfg.microbatch, max(1, len(self.pending)))
+            cap = self.cfg.microbatch
+            if self.cfg.spec_ramp:
+                cap = min(cap, max(1, len(self.pending)))
         else:
             cap = self.cfg.tree_cap
         cap = min(cap, 4, self.cfg.max_context - len(ctx))

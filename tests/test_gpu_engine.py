@@ -160,7 +160,8 @@ def test_randomized_stress_matches_serial(sp):
             draft_backend=["toy", "synthetic"][int(r.integers(0, 2))],
             alpha=float(r.choice([0.0, 0.3, 0.6, 0.9, 1.0])),
             microbatch=int(r.integers(1, 5)), partitions=int(r.integers(2, 9)),
-            continuous=bool(r.integers(0, 2)), cutoff=float(r.choice([0.0, 0.2, 0.5])),
+            continuous=bool(r.integers(0, 2)), spec_ramp=bool(i % 3),
+            cutoff=float(r.choice([0.0, 0.2, 0.5])),
             cutoff_recovery=float(r.choice([0.0, 0.05])),
             cutoff_decay=float(r.choice([0.0, 0.05])))
         res = sp.simulate(c)
