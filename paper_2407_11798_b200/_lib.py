@@ -14,7 +14,7 @@ import threading
 from .errors import CacheError, LibraryMissing, ModelError, ProtocolError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspecpipe_b200.so")
+LIB_PATH = os.environ.get("SP_LIB_PATH") or os.path.join(HERE, "libspecpipe_b200.so")  # override: A/B tools only
 
 # ---- status / flag constants (mirror the header) ---------------------------
 SP_OK, SP_ERR_MODEL, SP_ERR_CACHE, SP_ERR_PROTOCOL, SP_ERR_CUDA, SP_ERR_ARG, \

@@ -145,11 +145,37 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+  return ra;
+}
+// 4-byte store into a peer CTA's shared memory that completes (bytes) on
+// the peer's mbarrier
+__device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "r"(__float_as_uint(v)), "r"(rbar)
+               : "memory");
+}
+
 template <int ST>
 struct TcSmemTailT {
   uint64_t full[ST];
   uint64_t empty[ST];
   uint64_t done;
+  uint64_t red;             // push merge: the peers' partials have landed
   uint32_t tmem_base;
   int npre;                 // weight stages prefetched before the dependency wait
   int last;
@@ -163,7 +189,7 @@ struct TcSmemTailT {
 // GEMM is bounded by the bytes each SM keeps in flight
 template <int NT, int EPI, bool NORM, int ST>
 __global__ void __launch_bounds__(TC_THREADS)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const int push) {
   constexpr int XTILE = NT * TC_BK * 2;
   constexpr int STAGE = TC_WTILE + XTILE;
   constexpr uint32_t TMEM_COLS = NT < 32 ? 32 : NT;
@@ -189,6 +215,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
       mbar_init(&tail->empty[s], 1);
     }
     mbar_init(&tail->done, 1);
+    mbar_init(&tail->red, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
     // Weights do not depend on the previous kernel: start streaming the
@@ -219,13 +246,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tail->tmem_base;
+  // push merge: publish the initialised reduction barrier to the cluster
+  // now, wait for the peers' arrivals only when the partials are ready
+  if (push) cluster_arrive();
 
   // ---- programmatic dependency: everything below may read the previous
   // kernel's outputs (activations, run_state, norm statistics)
   pdl_wait();
   pdl_trigger();
   const int npre_done = tail->npre;
-  if (run_skipped(a.run_state)) {        // consistent for the whole grid
+  if (run_skipped(a.run_state)) {        // consistent for the whole grid (no one waits)
     if (threadIdx.x == 0) {              // drain the weight prefetch
       for (int i = 0; i < npre_done; ++i) {
         mbar_arrive(&tail->full[i]);
@@ -238,6 +268,33 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                    "r"(TMEM_COLS));
     return;
+  }
+
+  // epilogue operands that do not depend on this GEMM, loaded while it
+  // streams: per-token RMSNorm scales, the residual rows, the next gain
+  const int row = warp * 32 + lane;          // row within the tile
+  const int R = tile * TC_BM + row;          // global weight row
+  const int mv = min(NT, a.m - a.tok0);
+  const bool head = !push || split == 0;     // the CTA that runs the epilogue
+  if (NORM && head && threadIdx.x >= 64) {   // warps 2-3: not the producer / MMA lanes
+    for (int c = threadIdx.x - 64; c < mv; c += 64) {
+      float ssum = 0.f;
+      for (int p = 0; p < a.ss_nparts; ++p)
+        ssum = __fadd_rn(ssum, a.ss_in[(size_t)p * a.ss_ld + a.tok0 + c]);
+      tail->inv_rms[c] = rms_scale(ssum, a.k, a.norm_eps);
+    }
+  }
+  constexpr bool XEARLY = EPI == SP_EPI_RESID && NT <= 16;   // (registers)
+  float xold[XEARLY ? NT : 1];
+  float gnext = 1.0f;
+  if (EPI == SP_EPI_RESID && head) {
+    if (XEARLY) {
+      const float* x = reinterpret_cast<const float*>(a.out);
+#pragma unroll
+      for (int c = 0; c < (XEARLY ? NT : 0); ++c)
+        if (c < mv) xold[c] = x[(size_t)(a.tok0 + c) * a.ldo + R];
+    }
+    if (a.gain_next) gnext = a.gain_next[R];
   }
 
   if (warp == 0 && lane == 0) {
@@ -278,9 +335,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
   // ---- epilogue: TMEM -> registers (thread = weight row, NT token columns)
   mbar_wait(&tail->done, 0);
   tc_fence_after();
-  const int row = warp * 32 + lane;          // row within the tile
-  const int R = tile * TC_BM + row;          // global weight row
-  const int mv = min(NT, a.m - a.tok0);
   float acc[NT];
   if (nloc > 0) {
 #pragma unroll
@@ -296,7 +350,32 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
 
-  if (nsplit > 1) {
+  if (push) {
+    // split-K merge by push: the split CTAs of this row tile form one
+    // cluster; each peer stores its partial rows straight into rank 0's
+    // reduction buffer (st.async, completing on rank 0's barrier) and
+    // leaves; rank 0 sums them in split order and runs the epilogue
+    float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tail) +
+                                          sizeof(TcSmemTailT<ST>));   // [nsplit-1][mv][128]
+    cluster_wait();                      // rank 0's barrier is initialised
+    if (split != 0) {
+      const uint32_t rbar = map_rank(&tail->red, 0);
+      const uint32_t rbase = map_rank(red, 0);
+#pragma unroll
+      for (int c = 0; c < NT; ++c)
+        if (c < mv)
+          st_async_f32(rbase + (uint32_t)((((split - 1) * mv + c) * TC_BM + row) * 4), acc[c], rbar);
+      return;
+    }
+    if (threadIdx.x == 0)
+      mbar_expect_tx(&tail->red, (uint32_t)((nsplit - 1) * mv * TC_BM * 4));
+    mbar_wait(&tail->red, 0);
+    for (int sp2 = 1; sp2 < nsplit; ++sp2) {
+#pragma unroll
+      for (int c = 0; c < NT; ++c)
+        if (c < mv) acc[c] = __fadd_rn(acc[c], red[((sp2 - 1) * mv + c) * TC_BM + row]);
+    }
+  } else if (nsplit > 1) {
     // split-K merge through distributed shared memory: the nsplit CTAs of
     // this row tile form one cluster (grid y = cluster y); each parks its
     // partial in its own (now idle) stage buffers, rank 0 sums them in split
@@ -328,16 +407,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
     if (crank != 0) return;
   }
 
-  // per-token RMSNorm scale from the producer's sum-of-squares partials
-  if (NORM) {
-    if (threadIdx.x < mv) {
-      const int t = a.tok0 + threadIdx.x;
-      float s = 0.f;
-      for (int p = 0; p < a.ss_nparts; ++p) s = __fadd_rn(s, a.ss_in[(size_t)p * a.ss_ld + t]);
-      tail->inv_rms[threadIdx.x] = rms_scale(s, a.k, a.norm_eps);
-    }
-    __syncthreads();
-  }
+  // (per-token RMSNorm scales: computed before the main loop; the
+  // __syncthreads after the accumulator load published them)
 
   if (EPI == SP_EPI_QKV) {
     const int hd = a.head_dim;
@@ -388,7 +459,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
     }
   } else if (EPI == SP_EPI_RESID) {
     float* x = reinterpret_cast<float*>(a.out);
-    const float g = a.gain_next ? a.gain_next[R] : 1.0f;
+    const float g = gnext;
     float sq[NT];
 #pragma unroll
     for (int c = 0; c < NT; ++c) {
@@ -396,7 +467,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a) {
       if (c < mv) {
         const int t = a.tok0 + c;
         float* xp = x + (size_t)t * a.ldo + R;
-        const float nv = __fadd_rn(*xp, acc[c]);
+        const float nv = __fadd_rn(XEARLY ? xold[XEARLY ? c : 0] : *xp, acc[c]);
         *xp = nv;
         if (!isfinite(nv)) set_error(a.err, SP_DEV_NONFINITE);
         if (a.xb_next)
@@ -467,12 +538,19 @@ template <int NT, int EPI, bool NORM, int ST>
 static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
                              cudaStream_t st) {
   constexpr int STAGE = TC_WTILE + NT * TC_BK * 2;
-  const int smem = ST * STAGE + (int)sizeof(TcSmemTailT<ST>) + 1024;
-  static bool configured = false;
-  if (!configured) {
+  const int base = ST * STAGE + (int)sizeof(TcSmemTailT<ST>) + 1024;
+  // decode tiles merge split-K by push into a reduction buffer behind the
+  // tail ([ksplit-1][<=16 tokens][128 rows] f32) when it fits; prefill
+  // tiles (and oversize splits) pull from the peers after the main loop
+  const int red = NT == 16 && ksplit > 1 ? (ksplit - 1) * NT * TC_BM * 4 : 0;
+  static const bool nopush = getenv("SP_TC_PULL") != nullptr;   // experiments
+  const int push = red > 0 && !nopush && base + red <= 227 * 1024 ? 1 : 0;
+  const int smem = base + (push ? red : 0);
+  static int configured = 0;
+  if (configured < smem) {
     cudaFuncSetAttribute(tc_gemm_kernel<NT, EPI, NORM, ST>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
+    configured = smem;
   }
   dim3 grid(a.n_rows / TC_BM, ksplit);
   cudaLaunchConfig_t cfg = {};
@@ -489,7 +567,7 @@ static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<NT, EPI, NORM, ST>, x, a);
+  return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<NT, EPI, NORM, ST>, x, a, push);
 }
 
 template <int NT, int ST>
