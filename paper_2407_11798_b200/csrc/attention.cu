@@ -126,17 +126,50 @@ constexpr int ATT_UNROLL = 4;
 
 template <typename T, int HD>
 __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
-  pdl_wait();
-  pdl_trigger();
   constexpr int VEC = 16 / sizeof(T);
   constexpr int LPR = HD / VEC;           // lanes per row
   constexpr int G = ATT_THREADS / LPR;    // rows in flight per pass
   static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "bad head dim");
+  constexpr bool ONE = ATT_CH <= G * ATT_UNROLL;   // a split is one pass, K and V together
   __shared__ float sc[ATT_CH];
   extern __shared__ float mrg[];   // [nsplit][HD + 2] split partials (merging CTA)
   __shared__ float part[G][HD];
   __shared__ float red[ATT_THREADS / 32];
   __shared__ int last;
+
+  const int h = blockIdx.x, i = blockIdx.y;
+  const int kh = h / (a.H / a.KH);
+  const int kvd = a.KH * HD;
+  const int tid = threadIdx.x, g = tid / LPR, l = tid % LPR;
+  const int32_t* plan = a.vis + (size_t)i * a.ld_vis;
+  const T* Kc = reinterpret_cast<const T*>(a.k) + kh * HD + l * VEC;
+  const T* Vc = reinterpret_cast<const T*>(a.v) + kh * HD + l * VEC;
+
+  // Before the dependency wait: the plan (built at the start of the
+  // stage-run) and the K/V rows of cells older than this run are final;
+  // only rows >= fresh0 come from the QKV kernel this launch depends on.
+  // The old rows of this CTA's first split stream in while QKV drains.
+  const int fresh0 = a.fresh_row0_dev ? *a.fresh_row0_dev : a.fresh_row0;
+  const int len = a.vis_len[i];
+  const bool pre = ONE && fresh0 > 0 && !run_skipped(a.run_state);
+  uint4 kp[ATT_UNROLL], vp[ATT_UNROLL];
+  if (pre) {
+    const int e0 = blockIdx.z * ATT_CH, e1 = min(len, e0 + ATT_CH);
+#pragma unroll
+    for (int u = 0; u < ATT_UNROLL; ++u) {
+      const int e = e0 + u * G + g;
+      if (e < e1) {
+        const int row = plan[e];
+        if (row < fresh0) {
+          kp[u] = ld_stream16(Kc + (size_t)row * kvd);
+          vp[u] = ld_stream16(Vc + (size_t)row * kvd);
+        }
+      }
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (a.diag_empty) return;   // diagnostics: kernel-boundary cost only
 
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 &&
       a.cancel_word != nullptr && a.run_state_w != nullptr) {
@@ -146,16 +179,8 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
   }
   if (run_skipped(a.run_state)) return;
 
-  const int h = blockIdx.x, i = blockIdx.y;
-  const int len = a.vis_len[i];
   const int ns = (len + ATT_CH - 1) / ATT_CH;
   if (blockIdx.z == 0 && threadIdx.x == 0 && ns > a.nsplit) set_error(a.err, SP_DEV_PLAN_OVERFLOW);
-  const int kh = h / (a.H / a.KH);
-  const int kvd = a.KH * HD;
-  const int tid = threadIdx.x, g = tid / LPR, l = tid % LPR;
-  const int32_t* plan = a.vis + (size_t)i * a.ld_vis;
-  const T* Kc = reinterpret_cast<const T*>(a.k) + kh * HD + l * VEC;
-  const T* Vc = reinterpret_cast<const T*>(a.v) + kh * HD + l * VEC;
   const size_t obase = (size_t)i * a.H * HD + h * HD;
   auto store = [&](int d, float v) {
     if (a.out_bf16) reinterpret_cast<__nv_bfloat16*>(a.out)[obase + d] = __float2bfloat16_rn(v);
@@ -176,7 +201,6 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
     const int e0 = s * ATT_CH, e1 = min(len, e0 + ATT_CH);
     // a split fits one pass for bf16 heads: its V rows are loaded together
     // with its K rows (one round trip instead of two)
-    constexpr bool ONE = ATT_CH <= G * ATT_UNROLL;
     uint4 vpre[ATT_UNROLL];
     // scores
     for (int eb = e0; eb < e1; eb += G * ATT_UNROLL) {
@@ -185,8 +209,13 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
       for (int u = 0; u < ATT_UNROLL; ++u) {
         const int e = eb + u * G + g;
         const int row = e < e1 ? plan[e] : plan[e0];
-        kv[u] = ld_stream16(Kc + (size_t)row * kvd);
-        if (ONE) vpre[u] = ld_stream16(Vc + (size_t)row * kvd);
+        if (ONE && pre && s == (int)blockIdx.z && e < e1 && row < fresh0) {
+          kv[u] = kp[u];           // streamed before the dependency wait
+          vpre[u] = vp[u];
+        } else {
+          kv[u] = ld_stream16(Kc + (size_t)row * kvd);
+          if (ONE) vpre[u] = ld_stream16(Vc + (size_t)row * kvd);
+        }
       }
 #pragma unroll
       for (int u = 0; u < ATT_UNROLL; ++u) {
@@ -490,8 +519,14 @@ cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
                     run_state, hdr);
 }
 
-cudaError_t launch_attention(const AttnArgs& a, int kv_dtype, int hd,
+cudaError_t launch_attention(const AttnArgs& a0, int kv_dtype, int hd,
                              cudaStream_t st) {
+  static const bool nopre = getenv("SP_ATT_NOPRE") != nullptr;   // experiments
+  static const int diag = getenv("SP_ATT_DIAG") ? atoi(getenv("SP_ATT_DIAG")) : 0;
+  AttnArgs a = a0;
+  if (nopre) { a.fresh_row0_dev = nullptr; a.fresh_row0 = 0; }
+  if (diag == 2) return cudaSuccess;   // diagnostics: no attention launch at all
+  a.diag_empty = diag == 1;
   return kv_dtype == SP_DTYPE_BF16 ? attn_dispatch<__nv_bfloat16>(a, hd, st)
                                    : attn_dispatch<float>(a, hd, st);
 }

@@ -43,6 +43,11 @@ struct AttnArgs {
   int* err;
   int out_bf16;            // write the output as bf16 (tensor-core path input)
   int merge_smem;   // set by the launcher: merge partials through shared memory
+  // cache rows >= this are written by the kernel the launch depends on (the
+  // run's own cells); older rows may be read before the dependency wait
+  const int32_t* fresh_row0_dev;
+  int fresh_row0;
+  int diag_empty;   // diagnostics only (SP_ATT_DIAG=1): return after the dependency wait
 };
 
 struct LmPartial {
@@ -167,6 +172,36 @@ cudaError_t launch_compact_gather(const void* src, void* dst, const int32_t* src
                                   const int* live, int row_bytes, int n_max, cudaStream_t st);
 bool make_map_bf16(CUtensorMap* map, const void* base, long rows, long cols, long ld_elems,
                    int box_rows);
+// Persistent decode stage (stagemk.cu): every layer of a stage-run in one
+// cooperative launch, phases separated by grid barriers.
+struct MkLayer {
+  const void* qkv; const void* o; const void* up; const void* down;   // tiled bf16
+  const float* mlp_norm;     // gain of the MLP RMSNorm (O epilogue emits xb)
+  const float* gain_next;    // attn_norm of the next layer of the stage (or null)
+  void* kc; void* vc;        // this layer's K/V cell rows (bf16)
+};
+struct MkArgs {
+  const MkLayer* layers;
+  int nl, m;
+  int d, ffn, q_dim, kv_dim, head_dim, H, KH;
+  float eps, rope_theta, scale;
+  float* x;                  // residual stream f32 [m, d]
+  __nv_bfloat16* xb; __nv_bfloat16* attnb; __nv_bfloat16* hb;
+  float* q;
+  float* ss; int ss_ld, ss_parts0;
+  const sp_token* toks; const int32_t* row0_dev;
+  const int32_t* vis; const int32_t* vis_len; int ld_vis, nsplit;
+  float* att_scratch; int* att_tickets; int att_tstride;   // tickets one L2 line apart when room
+  float* scratch; int* tickets; int maxseg;                // (tile tickets: 16 ints apart)
+  int* run_state; const int* cancel_table; const RunHdr* hdr;
+  unsigned* bar;
+  int* err;
+  long long* prof;           // SP_MK_PROF: CTA 0's phase edges (site << 56 | clock64)
+};
+size_t stage_mk_smem();
+cudaError_t launch_stage_mk(const CUtensorMap& mxb, const CUtensorMap& mattn,
+                            const CUtensorMap& mhb, const MkArgs& a, int ctas, cudaStream_t st);
+
 cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st);
 int tc_nt_for(int m);
 int tc_ksplit(int n_rows, int k, int target_ctas);

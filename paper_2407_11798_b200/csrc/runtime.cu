@@ -294,6 +294,11 @@ struct sp_stage {
   long long* dprof = nullptr;            // SP_DRAFT_PROF: phase timestamps
   float* dxb = nullptr;
   float* dopart = nullptr;
+  // persistent decode stage (stagemk.cu)
+  MkLayer* mklayers = nullptr;           // device copy of the layer table
+  bool mk_dirty = true;
+  unsigned* mkbar = nullptr;             // grid barrier counter
+  int mk_maxseg = 0;
   // cell-pool compaction scratch (lazy)
   int32_t* cp_src = nullptr;
   int32_t* cp_pos = nullptr;
@@ -437,7 +442,8 @@ extern "C" int sp_stage_destroy(sp_stage* s) {
                   s->gate, s->hdr, s->xb, s->attnb, s->hb, s->ss,
                   s->tc_scratch, s->tc_tickets, s->gx_out, s->gres,
                   s->dlayers, s->dhdr, s->dbar, s->dprof, s->dxb, s->dopart,
-                  s->cp_src, s->cp_pos, s->cp_mask, s->cp_live, s->cp_rows};
+                  s->cp_src, s->cp_pos, s->cp_mask, s->cp_live, s->cp_rows,
+                  s->mklayers, s->mkbar};
   for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
   if (s->body_st) cudaStreamDestroy(s->body_st);
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -464,6 +470,7 @@ extern "C" int sp_stage_set_layer(sp_stage* s, int layer, const void* w_qkv,
   L.qkv = w_qkv; L.o = w_o; L.up = w_up; L.down = w_down;
   L.attn_norm = attn_norm; L.mlp_norm = mlp_norm;
   s->dlayers_dirty = true;
+  s->mk_dirty = true;
   return SP_OK;
 }
 
@@ -484,6 +491,7 @@ static void drop_graphs(sp_stage* s) {
 extern "C" int sp_stage_set_cta_budget(sp_stage* s, int ctas) {
   if (!s || ctas < 0) return SP_ERR_ARG;
   s->tc_ctas = ctas;
+  s->mk_dirty = true;   // the persistent stage's grid follows the budget
   drop_graphs(s);
   return SP_OK;
 }
@@ -546,6 +554,70 @@ struct HeadIO {            // fused LM head over the header's rows
   int update_tip = 0;
   int chain_gate = 0;
 };
+
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+// The persistent stage kernel (opt-in, SP_STAGE_MK=1) serves decode runs
+// (<= 16 tokens) of bf16 llama stages.  Parity-green, but not yet faster than
+// the one-GEMM-per-launch chain on the 7B stage.
+static bool mk_enabled(const sp_stage* s, int n) {
+  static const char* e = getenv("SP_STAGE_MK");
+  if (!e || atoi(e) == 0) return false;
+  const sp_model_dims& D = s->dims;
+  return s->tc && n <= 16 && (D.head_dim == 128 || D.head_dim == 64) && s->mk_maxseg > 0;
+}
+
+static int mk_ctas(const sp_stage* s) {
+  const int sms = sm_count();
+  const int c = s->tc_ctas > 0 ? s->tc_ctas / 2 : sms;
+  return c < 1 ? 1 : (c > sms ? sms : c);
+}
+
+// (Re)build the device layer table; sizes the stream-K merge slots.
+static int mk_prepare(sp_stage* s) {
+  if (!s->tc) return SP_OK;
+  const sp_model_dims& D = s->dims;
+  const int nl = s->hi - s->lo;
+  if (!s->mkbar) SP_CHECK(cudaMalloc((void**)&s->mkbar, sizeof(unsigned)));
+  if (!s->mklayers) SP_CHECK(cudaMalloc((void**)&s->mklayers, sizeof(MkLayer) * nl));
+  const size_t wb = wbytes(D);
+  std::vector<MkLayer> t(nl);
+  for (int i = 0; i < nl; ++i) {
+    const LayerW& L = s->layers[i];
+    t[i].qkv = L.qkv; t[i].o = L.o; t[i].up = L.up; t[i].down = L.down;
+    t[i].mlp_norm = L.mlp_norm;
+    t[i].gain_next = i + 1 < nl ? s->layers[i + 1].attn_norm : nullptr;
+    t[i].kc = (char*)s->kc + wb * s->kv_layer_elems * i;
+    t[i].vc = (char*)s->vc + wb * s->kv_layer_elems * i;
+  }
+  SP_CHECK(cudaMemcpy(s->mklayers, t.data(), sizeof(MkLayer) * nl, cudaMemcpyHostToDevice));
+  // merge slots: a tile of C chunks meets at most ceil(C / q) + 1 ranges
+  const int G = mk_ctas(s), d = D.d_model, f = D.ffn_dim;
+  const int shapes[4][2] = {{(s->q_dim + 2 * s->kv_dim) / 128, d / 64}, {d / 128, s->q_dim / 64},
+                            {2 * f / 128, d / 64}, {d / 128, f / 64}};
+  int maxseg = 1, maxtiles = 1;
+  for (auto& sh : shapes) {
+    const long total = (long)sh[0] * sh[1];
+    const long q = total / G;
+    if (q < 1) { s->mk_maxseg = 0; s->mk_dirty = false; return SP_OK; }   // too small a stage
+    const int segs = (int)((sh[1] + q - 1) / q) + 1;
+    maxseg = segs > maxseg ? segs : maxseg;
+    maxtiles = sh[0] > maxtiles ? sh[0] : maxtiles;
+  }
+  const bool fits = (size_t)maxtiles * maxseg * 16 * 128 <= (size_t)TC_SCRATCH_FLOATS &&
+                    maxtiles * 16 <= TC_TICKETS && maxseg <= 8;   // MK_MAXSEG
+  s->mk_maxseg = fits ? maxseg : 0;
+  s->mk_dirty = false;
+  return SP_OK;
+}
 
 // Enqueue one stage-run (layers [layer_a, layer_b)) reading every per-run
 // scalar from the device header.  ``graphable``: no host-dependent launch
@@ -645,7 +717,38 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
                         (const int*)s->run_state));
   }
   int ss_parts = 1;
-  for (int l = layer_a; l < layer_b; ++l) {
+  if (s->tc && s->mk_dirty) {   // layer table + merge slots (never inside a capture)
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+      const int rc = mk_prepare(s);
+      if (rc) return rc;
+    }
+  }
+  const bool mk = mk_enabled(s, n);
+  if (mk) {
+    MkArgs k{};
+    k.layers = s->mklayers + (layer_a - s->lo); k.nl = layer_b - layer_a; k.m = n;
+    k.d = d; k.ffn = D.ffn_dim; k.q_dim = s->q_dim; k.kv_dim = s->kv_dim;
+    k.head_dim = D.head_dim; k.H = D.n_heads; k.KH = D.n_kv_heads;
+    k.eps = D.norm_eps; k.rope_theta = D.rope_theta; k.scale = 1.0f / sqrtf((float)D.head_dim);
+    k.x = x_out; k.xb = s->xb; k.attnb = s->attnb; k.hb = s->hb; k.q = s->q;
+    k.ss = s->ss; k.ss_ld = s->max_tokens; k.ss_parts0 = 1;
+    k.toks = s->hdr_toks; k.row0_dev = row0_dev;
+    k.vis = s->vis; k.vis_len = s->vis_len; k.ld_vis = s->ld_vis; k.nsplit = nsplit;
+    k.att_scratch = s->att_scratch; k.att_tickets = s->att_tickets;
+    k.att_tstride = s->max_tokens >= 16 * 16 ? 16 : 1;   // (m <= 16 queries x H heads)
+    k.scratch = s->tc_scratch; k.tickets = s->tc_tickets; k.maxseg = s->mk_maxseg;
+    k.run_state = s->run_state; k.cancel_table = s->cancel_table; k.hdr = s->hdr;
+    k.bar = s->mkbar; k.err = s->err;
+    static const bool prof = getenv("SP_MK_PROF") != nullptr;
+    if (prof) {
+      if (!s->dprof) SP_CHECK(cudaMalloc((void**)&s->dprof, sizeof(long long) * 4096));
+      k.prof = s->dprof;
+    }
+    SP_CHECK(cudaMemsetAsync(s->mkbar, 0, sizeof(unsigned), st));
+    SP_CHECK(launch_stage_mk(s->m_xb[0], s->m_attnb[0], s->m_hb[0], k, mk_ctas(s), st));
+  }
+  for (int l = layer_a; l < (mk ? layer_a : layer_b); ++l) {
     const LayerW& L = s->layers[l - s->lo];
     void* kl = (char*)s->kc + wb * s->kv_layer_elems * (l - s->lo);
     void* vl = (char*)s->vc + wb * s->kv_layer_elems * (l - s->lo);
@@ -656,6 +759,7 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     a.out = s->attn; a.scratch = s->att_scratch; a.tickets = s->att_tickets;
     a.run_state = s->run_state; a.run_state_w = nullptr;
     a.cancel_word = nullptr; a.run_id = 0; a.err = s->err;
+    a.fresh_row0_dev = row0_dev;   // the QKV epilogue writes rows row0 .. row0 + n
     if (s->tc) {
       // ---- tensor-core path (tcgen05, bf16 activations, fp32 accumulate) ----
       TcArgs t{};

@@ -232,3 +232,30 @@ def test_stage_compact_moves_live_rows(sp):
     for r in range(6):
         k, v = st.read_kv_sync(1, r)
         assert np.array_equal(k, kv0[r][0]) and np.array_equal(v, kv0[r][1])
+
+
+def test_persistent_stage_kernel_streams(sp):
+    """The opt-in persistent decode stage (SP_STAGE_MK=1, one launch per
+    stage-run, grid barriers between phases, stream-K GEMMs) reproduces the
+    serial greedy stream in every mode (a subprocess: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import paper_2407_11798_b200 as sp\n"
+        "from paper_2407_11798_b200.engine import ExperimentConfig\n"
+        f"base = {DEEP!r}\n"
+        "for mode, nodes in [('iterative', 1), ('async-speculative', 4), ('sync-speculative', 3)]:\n"
+        "    c = ExperimentConfig(**{**base, 'mode': mode, 'nodes': nodes, 'gen_len': 24,\n"
+        "                            'prompt_len': 16, 'max_context': 512, 'prompt_seed': 5,\n"
+        "                            'target_seed': 7, 'draft_seed': 11,\n"
+        "                            'draft_backend': 'synthetic', 'alpha': 0.5})\n"
+        "    res = sp.simulate(c)\n"
+        "    ref = sp.reference_decode(c.target_config(), sp.sample_prompt(5, 16, c.vocab_size), 24)\n"
+        "    assert res.tokens == ref, mode\n"
+        "print('ok')\n")
+    env = dict(os.environ, SP_STAGE_MK="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

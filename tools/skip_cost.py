@@ -16,18 +16,21 @@ from paper_2407_11798_b200.pipeline import LocalPipeline
 cfg = sp.llama_config("llama2-7b")
 m = sp.build_model(cfg, torch.device("cuda", 0))
 pipe = LocalPipeline(m, [(0, 32)], partitions=8, capacity=4096, max_tokens=256)
-pre = [BatchToken(5 + i, i, frozenset([0]), i == 127) for i in range(128)]
-pipe.launch(1, 0, encode_tokens(pre), 0, [127])
-pipe.wait()
+CTX = int(os.environ.get("CTX", "128"))
+pre = [BatchToken(5 + (i % 100), i, frozenset([0]), i == CTX - 1) for i in range(CTX)]
+for c0 in range(0, CTX, 128):
+    chunk = pre[c0:c0 + 128]
+    pipe.launch(1 + c0, 0, encode_tokens(chunk), 0, [len(chunk) - 1])
+    pipe.wait()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 SPEC = _lib.SP_KIND_SPEC
 flags = _lib.SP_FWD_SKIPPABLE
 import time
 times = {"run": [], "skipped": [], "cancelled_at_1ms": []}
-rid = 2
+rid = 10000
 for rep in range(12):
     for kind in ("run", "skipped", "cancelled_at_1ms"):
-        toks = encode_tokens([BatchToken(7, 128 + rep, frozenset([1]), True)])
+        toks = encode_tokens([BatchToken(7, CTX + rep, frozenset([1]), True)])
         if kind == "skipped":
             pipe.cancel_run(rid)
         torch.cuda.synchronize()
