@@ -315,7 +315,20 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
     const float* base = a.scratch + ((size_t)i * a.H + h) * a.nsplit * (HD + 2);
     const float* src = base;
     if (a.merge_smem) {   // (else the partials are read from L2 directly)
-      for (int idx = tid; idx < ns * (HD + 2); idx += ATT_THREADS) mrg[idx] = __ldcg(base + idx);
+      const int tot = ns * (HD + 2);
+      for (int i0 = 0; i0 < tot; i0 += 8 * ATT_THREADS) {   // 8 loads in flight per thread
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int idx = i0 + k * ATT_THREADS + tid;
+          v[k] = idx < tot ? __ldcg(base + idx) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int idx = i0 + k * ATT_THREADS + tid;
+          if (idx < tot) mrg[idx] = v[k];
+        }
+      }
       __syncthreads();
       src = mrg;
     }

@@ -208,7 +208,8 @@ __device__ __forceinline__ void mk_epi_resid(const MkArgs& a, int tile, int R, i
 // ---------------------------------------------------------------------------
 template <int HD>
 __device__ void mk_attention(const MkArgs& a, const MkLayer& L, MkSmem* sm, int b, int G,
-                             int& pn) {
+                             int& pn, bool trace) {
+  int unit_k = 0;
   auto stamp = [&](int site) {
     if (a.prof && b == 0 && threadIdx.x == 96 && pn < 2040)
       a.prof[1 + pn++] = ((long long)site << 56) | (clock64() & ((1ll << 56) - 1));
@@ -329,6 +330,13 @@ __device__ void mk_attention(const MkArgs& a, const MkLayer& L, MkSmem* sm, int 
     }
     epi_sync();
     stamp(33);
+    if (trace && tid == 0 && unit_k < 4) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.prof[2048 + 512 + b * 8 + 2 * unit_k] = t;
+      a.prof[2048 + 512 + b * 8 + 2 * unit_k + 1] = sm->last;
+      ++unit_k;
+    }
     if (sm->last) {
       __threadfence();
       // all partials of this (query, head) in one coalesced round trip, then
@@ -337,7 +345,20 @@ __device__ void mk_attention(const MkArgs& a, const MkLayer& L, MkSmem* sm, int 
       const bool staged = ns * (HD + 2) <= MK_MRG;
       const float* src = base;
       if (staged) {
-        for (int idx = tid; idx < ns * (HD + 2); idx += MK_EPI_THREADS) sm->mrg[idx] = __ldcg(base + idx);
+        const int tot = ns * (HD + 2);
+        for (int i0 = 0; i0 < tot; i0 += 8 * MK_EPI_THREADS) {   // 8 loads in flight per thread
+          float v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int idx = i0 + k * MK_EPI_THREADS + tid;
+            v[k] = idx < tot ? __ldcg(base + idx) : 0.f;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int idx = i0 + k * MK_EPI_THREADS + tid;
+            if (idx < tot) sm->mrg[idx] = v[k];
+          }
+        }
         epi_sync();
         src = sm->mrg;
       }
@@ -535,7 +556,7 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
           if (ph == PH_ATTN) {
             long long t0 = 0;
             if (a.prof && l == 5 && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-            mk_attention<HD>(a, L, sm, b, G, pn);
+            mk_attention<HD>(a, L, sm, b, G, pn, a.prof && l == 5);
             if (a.prof && l == 5 && tid == 0) {
               long long t1;
               asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));

@@ -64,3 +64,8 @@ print("layer-5 attention per CTA (us from first start): start min/max %.2f/%.2f 
       % (0, (t0.max() - base) / 1e3, (t1.min() - base) / 1e3, np.median(t1 - base) / 1e3, (t1.max() - base) / 1e3))
 order = np.argsort(t1)[-8:]
 print("slowest CTAs:", [(int(c), round((t1[c] - base) / 1e3, 2)) for c in order])
+
+u = allraw[2047 + 512:2047 + 512 + 148 * 8].reshape(148, 8)
+for c in list(order[-4:]) + [0, 1]:
+    ends = [(round((u[c, 2 * k] - base) / 1e3, 2), int(u[c, 2 * k + 1])) for k in range(4) if u[c, 2 * k] > 0]
+    print("CTA", int(c), "unit ends (us, merged?)", ends, "attn end", round((t1[c] - base) / 1e3, 2))
