@@ -302,7 +302,8 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
     out = eng.generate(prompt)
     e2e_s = time.perf_counter() - t0
     rf = gemv_roofline(eng)
-    cpu = cpu_baseline() if not args.no_cpu else None
+    # the CPU baseline is timed on rank 0 at N=1 only (the bench contract)
+    cpu = cpu_baseline() if not args.no_cpu and n_gpus == 1 else None
     wb = eng.target.config.weight_bytes()
     return {
         "metric": "single-request generated tokens/s + inter-token latency",
