@@ -44,9 +44,12 @@ struct TcSmemTailT {
 };
 
 // ---- the kernel -------------------------------------------------------------
-// ST = ring depth: 4 stages (2 CTAs/SM) for wide grids, 10 (one CTA/SM,
-// 160 KB of weights in flight) when the grid fits one CTA per SM -- a decode
-// GEMM is bounded by the bytes each SM keeps in flight
+// ST = ring depth: 5 stages (2 CTAs/SM) for wide grids, 6 when the grid
+// fits one CTA per SM.  Deeper rings were measured slower in the layer chain
+// (7B stage-run: deep 10 -> 6 stages 2.71 -> 2.67 ms, 12 stages 2.74;
+// shallow 4 -> 5 stages 2.67 -> 2.63 ms, 3 stages 2.93): a smaller footprint
+// lets the next GEMM's CTAs become resident -- and prefetch their weights
+// before the dependency wait -- while this one drains
 template <int NT, int EPI, bool NORM, int ST>
 __global__ void __launch_bounds__(TC_THREADS)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const int push) {
@@ -412,7 +415,8 @@ static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
   // decode tiles merge split-K by push into a reduction buffer behind the
   // tail ([ksplit-1][<=16 tokens][128 rows] f32) when it fits; prefill
   // tiles (and oversize splits) pull from the peers after the main loop
-  const int red = NT == 16 && ksplit > 1 ? (ksplit - 1) * NT * TC_BM * 4 : 0;
+  const int mvl = a.m - a.tok0 < NT ? a.m - a.tok0 : NT;   // token columns of this tile
+  const int red = NT == 16 && ksplit > 1 ? (ksplit - 1) * mvl * TC_BM * 4 : 0;
   static const bool nopush = getenv("SP_TC_PULL") != nullptr;   // experiments
   const int push = red > 0 && !nopush && base + red <= 227 * 1024 ? 1 : 0;
   const int smem = base + (push ? red : 0);
@@ -475,6 +479,17 @@ int tc_ksplit(int n_rows, int k, int target_ctas) {
   return ks;
 }
 
+// ring depths (see tc_gemm_kernel); SP_TC_DEEP_ST=4..8|10 and
+// SP_TC_SHALLOW_ST=3..5 select others for experiments
+static int deep_st() {
+  static const int v = getenv("SP_TC_DEEP_ST") ? atoi(getenv("SP_TC_DEEP_ST")) : 6;
+  return v;
+}
+static int shallow_st() {
+  static const int v = getenv("SP_TC_SHALLOW_ST") ? atoi(getenv("SP_TC_SHALLOW_ST")) : 5;
+  return v;
+}
+
 // Launch over all tokens (token tiles of NT); maps[0] is the NT=16 X map,
 // maps[1] the NT=128 one.
 cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st) {
@@ -502,8 +517,15 @@ cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st) 
     a.tok0 = t0;
     cudaError_t e;
     if (nt == 16)
-      e = deep ? launch_epi<16, 10>(xmaps[0], a, ksplit, st)
-               : launch_epi<16, 4>(xmaps[0], a, ksplit, st);
+      e = !deep ? (shallow_st() == 3   ? launch_epi<16, 3>(xmaps[0], a, ksplit, st)
+                   : shallow_st() == 5 ? launch_epi<16, 5>(xmaps[0], a, ksplit, st)
+                                       : launch_epi<16, 4>(xmaps[0], a, ksplit, st))
+          : deep_st() == 7 ? launch_epi<16, 7>(xmaps[0], a, ksplit, st)
+          : deep_st() == 8 ? launch_epi<16, 8>(xmaps[0], a, ksplit, st)
+          : deep_st() == 6 ? launch_epi<16, 6>(xmaps[0], a, ksplit, st)
+          : deep_st() == 5 ? launch_epi<16, 5>(xmaps[0], a, ksplit, st)
+          : deep_st() == 4 ? launch_epi<16, 4>(xmaps[0], a, ksplit, st)
+                           : launch_epi<16, 10>(xmaps[0], a, ksplit, st);
     else
       e = launch_epi<128, 4>(xmaps[1], a, ksplit, st);
     if (e != cudaSuccess) return e;
