@@ -231,3 +231,33 @@ def test_llama_small_matches_oracle(sp):
         g, o = dec.feed([t]), odec.feed([t])
         errs.append(np.abs(g - o).max())
     assert max(errs) < BF16_TOL, errs
+
+
+@pytest.mark.parametrize("shape,tiled", [("llama2-13b", True), ("llama2-70b", True),
+                                         ("tinyllama-1.1b", False), ("tinyllama-1.1b", True)])
+def test_llama_config_widths_match_oracle(sp, shape, tiled):
+    """The BASELINE configs' model widths (13B / 70B targets on the tcgen05
+    path; the 1.1B draft on the SWZ8 GEMV path and tiled): a 1-layer slice
+    at the real width, vocabulary and head layout (70B: GQA 64/8 heads,
+    1.1B: 32/4 at head dim 64) against the fp64 oracle on the same weights --
+    prompt logits and greedy decode steps within the bf16 tolerance."""
+    from oracle import model as OM
+    cfg = sp.llama_config(shape, max_context=64, seed=3, n_layers=1)
+    m = sp.build_model(cfg, tiled=tiled)
+    nat = m.natural_weights()
+    oc = OM.OracleConfig(vocab_size=cfg.vocab_size, embed_dim=cfg.embed_dim, n_layers=1,
+                         n_heads=cfg.n_heads, max_context=64, seed=3, arch="llama",
+                         n_kv_heads=cfg.n_kv_heads, ffn_dim=cfg.ffn_dim)
+    om = OM.OracleModel(oc, nat["embedding"], None, nat["layers"], nat["w_out"],
+                        nat["final_norm"])
+    prompt = sp.sample_prompt(4, 6, cfg.vocab_size)
+    dec = sp.SerialDecoder(m, full_logits=True)
+    odec = OM.OracleDecoder(om)
+    g = dec.feed(prompt)
+    o = odec.feed(prompt)
+    errs = [np.abs(g - o).max()]
+    for _ in range(2):
+        t = int(np.argmax(o))
+        g, o = dec.feed([t]), odec.feed([t])
+        errs.append(np.abs(g - o).max())
+    assert max(errs) < BF16_TOL, errs
