@@ -193,7 +193,7 @@ def test_async_head_randomized_matches_serial(world):
             partitions=int(r.integers(2, 9)), microbatch=int(r.integers(1, 5)),
             continuous=bool(r.integers(0, 2)), alpha=float(r.choice([0.0, 0.4, 0.8, 1.0])),
             cutoff=float(r.choice([0.0, 0.3])), cutoff_recovery=float(r.choice([0.0, 0.05])),
-            cutoff_decay=float(r.choice([0.0, 0.05])))
+            cutoff_decay=float(r.choice([0.0, 0.05])), spec_ramp=trial % 4 != 3)
         pipe = FakePipeline(om, plan_layer_split(4, nodes - 1), cfg.partitions, r)
         draft = FakeDraft(truth, runner, cfg.alpha, trial, 96, r)
         head = Head(cfg, pipe, draft, prompt, 16)
@@ -239,3 +239,34 @@ def test_f4b_backoff_refeeds_tip(world):
     head.mirror = list(prompt) + [5, 6, 7]
     assert head._backoff(len(prompt), list(prompt)) == (len(prompt) - 1, [prompt[-1]])
     assert head._backoff(len(prompt) - 2, list(prompt)) == (len(prompt) - 2, prompt[-2:])
+
+
+def test_spec_ramp_caps_requests(world):
+    """The reference's continuous micro-batch ramp (engine.py:1027-1030): a
+    fresh chain asks the draft for one token, deeper chains up to
+    ``microbatch``; spec_ramp=False always asks for ``microbatch``."""
+    om, streams = world
+    prompt, truth, runner = streams[0]
+    caps = {}
+    for ramp in (True, False):
+        cfg = ExperimentConfig(mode="async-speculative", nodes=2, vocab_size=16, embed_dim=16,
+                               target_layers=4, max_context=96, prompt_len=8, gen_len=24,
+                               microbatch=4, alpha=1.0, cutoff=0.0, spec_ramp=ramp)
+        r = np.random.Generator(np.random.PCG64(1))
+        pipe = FakePipeline(om, [(0, 4)], cfg.partitions, r)
+        draft = FakeDraft(truth, runner, cfg.alpha, 0, 96, r)
+        head = Head(cfg, pipe, draft, prompt, 16)
+        seen = []
+        orig = head._draft_request
+
+        def spy(truncate_to, feed, max_tokens, cutoff, _orig=orig, _seen=seen):
+            _seen.append(max_tokens)
+            return _orig(truncate_to, feed, max_tokens, cutoff)
+
+        head._draft_request = spy
+        head.run_async_speculative()
+        assert head.accepted[len(prompt):] == truth[len(prompt):len(prompt) + 24]
+        caps[ramp] = seen
+    ramp, flat = [c for c in caps[True] if c > 0], [c for c in caps[False] if c > 0]  # (0: prefill feed)
+    assert ramp[0] == 1 and all(1 <= c <= 4 for c in ramp)
+    assert set(flat) == {4}
