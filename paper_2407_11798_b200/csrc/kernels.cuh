@@ -199,6 +199,7 @@ struct MkArgs {
   long long* prof;           // SP_MK_PROF: CTA 0's phase edges (site << 56 | clock64)
 };
 size_t stage_mk_smem();
+void stage_mk_occupancy_report();
 cudaError_t launch_stage_mk(const CUtensorMap& mxb, const CUtensorMap& mattn,
                             const CUtensorMap& mhb, const MkArgs& a, int ctas, cudaStream_t st);
 

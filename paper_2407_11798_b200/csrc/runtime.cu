@@ -577,6 +577,8 @@ static bool mk_enabled(const sp_stage* s, int n) {
 }
 
 static int mk_ctas(const sp_stage* s) {
+  static bool reported = false;
+  if (!reported && getenv("SP_MK_VERBOSE")) { reported = true; stage_mk_occupancy_report(); }
   const int sms = sm_count();
   const int c = s->tc_ctas > 0 ? s->tc_ctas / 2 : sms;
   return c < 1 ? 1 : (c > sms ? sms : c);

@@ -27,6 +27,7 @@
 // (model.py:188-189) as a per-token scale from sum-of-squares partials;
 // early cancellation between layers (engine.py:602-612).
 #include <cuda.h>
+#include <cstdio>
 
 #include "gemv_core.cuh"
 #include "kernels.cuh"
@@ -679,6 +680,25 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
 }
 
 size_t stage_mk_smem() { return MK_ST * MK_STAGE + sizeof(MkSmem) + 1024; }
+
+// diagnostics (SP_MK_VERBOSE): co-residency of the persistent kernel
+void stage_mk_occupancy_report() {
+  auto kern = stage_mk_kernel<128>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const int smems[4] = {0, 16 * 1024, 64 * 1024, 100 * 1024};
+  const int thr[3] = {128, 224, 256};
+  for (int t : thr)
+    for (int sm : smems) {
+      int n = -1;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, t, sm);
+      fprintf(stderr, "stage_mk occupancy: threads %d smem %d -> %d CTAs/SM (%s)\n", t, sm, n,
+              cudaGetErrorString(e));
+    }
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, kern);
+  fprintf(stderr, "stage_mk attrs: regs %d local %zu const %zu maxThreads %d\n", fa.numRegs,
+          fa.localSizeBytes, fa.constSizeBytes, fa.maxThreadsPerBlock);
+}
 
 cudaError_t launch_stage_mk(const CUtensorMap& mxb, const CUtensorMap& mattn,
                             const CUtensorMap& mhb, const MkArgs& a, int ctas, cudaStream_t st) {
