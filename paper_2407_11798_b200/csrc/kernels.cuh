@@ -205,6 +205,7 @@ cudaError_t launch_stage_mk(const CUtensorMap& mxb, const CUtensorMap& mattn,
 
 cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st);
 int tc_nt_for(int m);
+int tc_gemm_occupancy();
 int tc_ksplit(int n_rows, int k, int target_ctas);
 
 }  // namespace sp

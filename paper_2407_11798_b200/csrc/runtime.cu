@@ -577,6 +577,8 @@ static bool mk_enabled(const sp_stage* s, int n) {
 }
 
 static int mk_ctas(const sp_stage* s) {
+  static const bool noncoop = getenv("SP_MK_NONCOOP") != nullptr;
+  if (noncoop) return 2 * sm_count();
   static bool reported = false;
   if (!reported && getenv("SP_MK_VERBOSE")) { reported = true; stage_mk_occupancy_report(); }
   const int sms = sm_count();
@@ -616,7 +618,7 @@ static int mk_prepare(sp_stage* s) {
     maxtiles = sh[0] > maxtiles ? sh[0] : maxtiles;
   }
   const bool fits = (size_t)maxtiles * maxseg * 16 * 128 <= (size_t)TC_SCRATCH_FLOATS &&
-                    maxtiles * 16 <= TC_TICKETS && maxseg <= 8;   // MK_MAXSEG
+                    maxtiles * 16 <= TC_TICKETS && maxseg <= 16;   // MK_MAXSEG
   s->mk_maxseg = fits ? maxseg : 0;
   s->mk_dirty = false;
   return SP_OK;
@@ -745,7 +747,7 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     k.bar = s->mkbar; k.err = s->err;
     static const bool prof = getenv("SP_MK_PROF") != nullptr;
     if (prof) {
-      if (!s->dprof) SP_CHECK(cudaMalloc((void**)&s->dprof, sizeof(long long) * 4096));
+      if (!s->dprof) SP_CHECK(cudaMalloc((void**)&s->dprof, sizeof(long long) * 16384));
       k.prof = s->dprof;
     }
     SP_CHECK(cudaMemsetAsync(s->mkbar, 0, sizeof(unsigned), st));
@@ -1447,7 +1449,7 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
   a.xb = s->dxb; a.opart = s->dopart;
   a.out = out; a.err = s->err; a.err_out = err_out;
   if (getenv("SP_DRAFT_PROF")) {
-    if (!s->dprof) SP_CHECK(cudaMalloc((void**)&s->dprof, sizeof(long long) * 4096));
+    if (!s->dprof) SP_CHECK(cudaMalloc((void**)&s->dprof, sizeof(long long) * 16384));
     a.prof = s->dprof;
   }
   a.spin_ns = getenv("SP_DRAFT_SPIN_NS") ? (unsigned)atoi(getenv("SP_DRAFT_SPIN_NS")) : 32u;

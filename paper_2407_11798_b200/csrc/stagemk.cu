@@ -36,9 +36,15 @@
 namespace sp {
 
 constexpr int MK_THREADS = 224;   // 7 warps
-constexpr int MK_ST = 10;         // ring slots of (16 KB weights + 2 KB activations)
-constexpr int MK_MRG = 8192;      // attention merge staging (floats): 63 splits at HD 128
-constexpr int MK_MAXSEG = 8;      // stream-K segments per tile merged from registers
+#ifndef MK_ST_DEF
+#define MK_ST_DEF 10
+#endif
+constexpr int MK_ST = MK_ST_DEF;   // ring slots of (16 KB weights + 2 KB activations)
+#ifndef MK_MRG_DEF
+#define MK_MRG_DEF 8192
+#endif
+constexpr int MK_MRG = MK_MRG_DEF; // attention merge staging (floats): 63 splits at HD 128
+constexpr int MK_MAXSEG = 16;     // stream-K segments per tile merged from registers
 constexpr int MK_NT = 16;         // token columns (UMMA_N)
 constexpr int MK_XTILE = MK_NT * TC_BK * 2;
 constexpr int MK_STAGE = TC_WTILE + MK_XTILE;
@@ -334,8 +340,8 @@ __device__ void mk_attention(const MkArgs& a, const MkLayer& L, MkSmem* sm, int 
     if (trace && tid == 0 && unit_k < 4) {
       long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.prof[2048 + 512 + b * 8 + 2 * unit_k] = t;
-      a.prof[2048 + 512 + b * 8 + 2 * unit_k + 1] = sm->last;
+      a.prof[4096 + 1024 + b * 8 + 2 * unit_k] = t;
+      a.prof[4096 + 1024 + b * 8 + 2 * unit_k + 1] = sm->last;
       ++unit_k;
     }
     if (sm->last) {
@@ -561,8 +567,8 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
             if (a.prof && l == 5 && tid == 0) {
               long long t1;
               asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-              a.prof[2048 + b] = t0;
-              a.prof[2048 + 256 + b] = t1;
+              a.prof[4096 + b] = t0;
+              a.prof[4096 + 512 + b] = t1;
             }
           } else {
             const MkGemm gm = mk_gemm(a, L, ph);
@@ -650,6 +656,11 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
           epi_sync();
           if (a.prof && b == 0 && tid == 0 && pn < 2040)   // phase work done
             a.prof[1 + pn++] = ((long long)(20 + ph) << 56) | (clock64() & ((1ll << 56) - 1));
+          if (a.prof && l == 5 && tid == 0 && b < 512) {   // per-CTA phase end (ns)
+            long long tg;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg));
+            a.prof[10240 + ph * 512 + b] = tg;
+          }
           if (tid == 0) {
             __threadfence();
             if (ph == PH_DOWN && b == 0 && l + 1 < a.nl && a.cancel_table) {
@@ -663,7 +674,7 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
         }
       }
     }
-    if (a.prof && b == 0 && tid == 0) { a.prof[0] = 4094; a.prof[4094] = pn; }
+    if (a.prof && b == 0 && tid == 0) { a.prof[0] = 16382; a.prof[16382] = pn; }
     if (tid == 0) sm->stop = 1;    // release any role still waiting
   }
 
@@ -694,6 +705,7 @@ void stage_mk_occupancy_report() {
       fprintf(stderr, "stage_mk occupancy: threads %d smem %d -> %d CTAs/SM (%s)\n", t, sm, n,
               cudaGetErrorString(e));
     }
+  fprintf(stderr, "tc_gemm<16,QKV,norm,5> occupancy API: %d CTAs/SM\n", tc_gemm_occupancy());
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, kern);
   fprintf(stderr, "stage_mk attrs: regs %d local %zu const %zu maxThreads %d\n", fa.numRegs,
@@ -717,7 +729,10 @@ cudaError_t launch_stage_mk(const CUtensorMap& mxb, const CUtensorMap& mattn,
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;   // co-residency for the grid barriers
-  attr[0].val.cooperative = 1;
+  // (the occupancy API counts a TMEM kernel as one CTA per SM; SP_MK_NONCOOP=1
+  // launches two per SM without the guarantee -- experiments only)
+  static const bool noncoop = getenv("SP_MK_NONCOOP") != nullptr;
+  attr[0].val.cooperative = noncoop ? 0 : 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;

@@ -465,6 +465,17 @@ static cudaError_t launch_epi(const CUtensorMap& x, const TcArgs& a, int ksplit,
 
 int tc_nt_for(int m) { return m <= 16 ? 16 : 128; }
 
+// diagnostics: the occupancy API's view of a decode GEMM instance
+int tc_gemm_occupancy() {
+  auto kern = tc_gemm_kernel<16, SP_EPI_QKV, true, 5>;
+  constexpr int STAGE = TC_WTILE + 16 * TC_BK * 2;
+  const int smem = 5 * STAGE + (int)sizeof(TcSmemTailT<5>) + 1024;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int n = -1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, TC_THREADS, smem);
+  return n;
+}
+
 // Split-K factor: as many CTAs as fit in ONE wave (a second partial wave
 // doubles the tail) but at least 16 chunks (256 KB of weights) per CTA so
 // the fixed prologue/merge cost is amortised (measured on the 7B shapes:

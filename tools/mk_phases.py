@@ -27,10 +27,10 @@ for rep in range(4):
     pipe.launch(1000 + rep, 1, encode_tokens([BatchToken(7, ctx + rep, frozenset([0]), True)]), 0, [0])
     pipe.wait()
 st = pipe.stages[0]
-buf = (C.c_longlong * 4096)()
-n_all = st.lib.sp_stage_draft_profile(st.h, buf, 4096)
+buf = (C.c_longlong * 16384)()
+n_all = st.lib.sp_stage_draft_profile(st.h, buf, 16383)
 allraw = np.array(buf[:n_all], dtype=np.int64)
-n = int(allraw[4093])
+n = int(allraw[16381])
 raw = allraw[:n]
 site = raw >> 56
 clk = raw & ((1 << 56) - 1)
@@ -57,15 +57,21 @@ for k in NAMES:
     print(f"  {k:5s} work mean {w.mean():6.2f} us (total {w.sum():7.1f})   "
           f"barrier-wait before it mean {b.mean():6.2f} us (total {b.sum():7.1f})")
 
-t0 = allraw[2047:2047 + 148]
-t1 = allraw[2047 + 256:2047 + 256 + 148]
+G = int(os.environ.get("MK_G", "148"))
+t0 = allraw[4095:4095 + G]
+t1 = allraw[4095 + 512:4095 + 512 + G]
 base = t0.min()
 print("layer-5 attention per CTA (us from first start): start min/max %.2f/%.2f  end min/median/max %.2f/%.2f/%.2f"
       % (0, (t0.max() - base) / 1e3, (t1.min() - base) / 1e3, np.median(t1 - base) / 1e3, (t1.max() - base) / 1e3))
 order = np.argsort(t1)[-8:]
 print("slowest CTAs:", [(int(c), round((t1[c] - base) / 1e3, 2)) for c in order])
 
-u = allraw[2047 + 512:2047 + 512 + 148 * 8].reshape(148, 8)
+u = allraw[4095 + 1024:4095 + 1024 + G * 8].reshape(G, 8)
 for c in list(order[-4:]) + [0, 1]:
     ends = [(round((u[c, 2 * k] - base) / 1e3, 2), int(u[c, 2 * k + 1])) for k in range(4) if u[c, 2 * k] > 0]
     print("CTA", int(c), "unit ends (us, merged?)", ends, "attn end", round((t1[c] - base) / 1e3, 2))
+
+pe = allraw[10239:10239 + 5 * 512].reshape(5, 512)[:, :G]
+for ph, name in enumerate(NAMES):
+    v = (pe[ph] - pe[ph].min()) / 1e3
+    print(f"layer-5 {name:5s} per-CTA end spread: median {np.median(v):5.2f} p90 {np.percentile(v, 90):5.2f} max {v.max():5.2f} us; latest CTAs {list(np.argsort(v)[-5:])}")
