@@ -541,7 +541,7 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
     const int tq = warp & 3;                 // TMEM lane quarter = warp % 4
     const int row = tq * 32 + lane;          // row within the tile
     const int tid = threadIdx.x - 96;
-    int seg = 0, pn = 0;
+    int seg = 0, pn = 0, nmerge = 0;
     float acc[MK_NT];
     if (!skipped) {
       for (int l = 0; l < a.nl; ++l) {
@@ -558,6 +558,7 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
             if (tid == 0) mk_wait_epoch(a.bar, (unsigned)G * (MK_PH * l + ph));
             epi_sync();
           }
+          nmerge = 0;
           if (a.prof && b == 0 && tid == 0 && pn < 2040)   // phase start (barrier passed)
             a.prof[1 + pn++] = ((long long)(10 + ph) << 56) | (clock64() & ((1ll << 56) - 1));
           if (ph == PH_ATTN) {
@@ -616,6 +617,7 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
                 epi_sync();
                 mine = sm->last != 0;
                 if (mine) {
+                  ++nmerge;
                   __threadfence();
                   // K order: segments 0..nseg-1 (own partial from registers);
                   // every peer partial of a token column in flight at once
@@ -660,6 +662,7 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
             long long tg;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg));
             a.prof[10240 + ph * 512 + b] = tg;
+            a.prof[12800 + ph * 512 + b] = nmerge;
           }
           if (tid == 0) {
             __threadfence();

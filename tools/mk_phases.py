@@ -75,3 +75,10 @@ pe = allraw[10239:10239 + 5 * 512].reshape(5, 512)[:, :G]
 for ph, name in enumerate(NAMES):
     v = (pe[ph] - pe[ph].min()) / 1e3
     print(f"layer-5 {name:5s} per-CTA end spread: median {np.median(v):5.2f} p90 {np.percentile(v, 90):5.2f} max {v.max():5.2f} us; latest CTAs {list(np.argsort(v)[-5:])}")
+
+nm = allraw[12799:12799 + 5 * 512].reshape(5, 512)[:, :G]
+for ph, name in enumerate(NAMES):
+    v = (pe[ph] - pe[ph].min()) / 1e3
+    late = v > np.percentile(v, 90)
+    print(f"  {name:5s} merges per CTA: late (p90+) mean {nm[ph][late].mean():.2f}, others {nm[ph][~late].mean():.2f};"
+          f" late CTAs b<148: {int((np.where(late)[0] < 148).sum())}/{int(late.sum())}")
