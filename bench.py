@@ -101,6 +101,18 @@ class Clocks:
 # ---------------------------------------------------------------------------
 
 def cpu_baseline(n_decode: int = 3, layers: int = 2, prompt_len: int = 16) -> dict:
+    """The oracle's fp64 forward timed with every host thread BLAS can use
+    (torchrun exports OMP_NUM_THREADS=1; the reference arm must not inherit it)."""
+    import numpy  # noqa: F401  (load BLAS first: threadpoolctl only sees loaded libraries)
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=os.cpu_count() or 1):
+            return _cpu_baseline(n_decode, layers, prompt_len)
+    except ImportError:
+        return _cpu_baseline(n_decode, layers, prompt_len)
+
+
+def _cpu_baseline(n_decode: int, layers: int, prompt_len: int) -> dict:
     import numpy as np
     from oracle import model as OM
     from oracle.kvcache import OracleCache
