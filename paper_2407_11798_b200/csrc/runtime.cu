@@ -49,6 +49,44 @@ __global__ void embed_kernel(const T* __restrict__ emb,
   }
 }
 
+// K1 fused with the tensor-core path's stage input (bf16-only stages whose
+// first layer is layer 0): x = E[tok] and, from the same registers, the
+// RMSNorm statistic (fixed-order block reduction) and xb = bf16(x * gain) --
+// the exact arithmetic of embed_kernel followed by prep_kernel at 256 threads.
+__global__ void embed_prep_kernel(const __nv_bfloat16* __restrict__ emb,
+                                  const sp_token* __restrict__ toks, int d, int vocab,
+                                  int max_context, float* __restrict__ x,
+                                  const float* __restrict__ gain, __nv_bfloat16* __restrict__ xb,
+                                  float* __restrict__ ss, int* err, const int* run_state) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[8];
+  if (run_skipped(run_state)) return;
+  const int i = blockIdx.x;
+  const sp_token t = toks[i];
+  const bool ok_t = t.token >= 0 && t.token < vocab;
+  const bool ok_p = t.pos >= 0 && t.pos < max_context;
+  if (threadIdx.x == 0) {
+    if (!ok_t) set_error(err, SP_DEV_BAD_TOKEN);
+    if (!ok_p) set_error(err, SP_DEV_BAD_POS);
+  }
+  float s = 0.f;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    const float v = ok_t ? to_f32(emb[(size_t)t.token * d + c]) : 0.f;
+    x[(size_t)i * d + c] = v;
+    s = __fmaf_rn(v, v, s);
+    xb[(size_t)i * d + c] = __float2bfloat16_rn(gain ? __fmul_rn(v, gain[c]) : v);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) tot = __fadd_rn(tot, red[w]);
+    ss[i] = tot;
+  }
+}
+
 // Stage-run prologue: fold cancel word / upstream placeholder / draft-chain
 // gate into run_state, take token 0 from the chain if asked, write metadata.
 // Every per-run scalar comes from the device run header, so the same launch
@@ -673,7 +711,14 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     st = body_st;
   }
   void* stream = reinterpret_cast<void*>(st);
-  if (layer_a == 0) {
+  // tensor-core stages starting at layer 0: embedding + stage input in one pass
+  const bool fused_prep = s->tc && layer_a == 0 && s->pos_table == nullptr && d >= 256;
+  if (fused_prep) {
+    SP_CHECK(launch_pdl(embed_prep_kernel, dim3(n), dim3(256), 0, st,
+                        (const __nv_bfloat16*)s->emb, (const sp_token*)s->hdr_toks, d, D.vocab,
+                        D.max_context, io.x_out, s->layers[0].attn_norm, s->xb, s->ss, s->err,
+                        (const int*)s->run_state));
+  } else if (layer_a == 0) {
     const int threads = d >= 256 ? 256 : 64;
     if (D.w_dtype == SP_DTYPE_BF16)
       SP_CHECK(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(n), dim3(threads), 0, st,
@@ -715,7 +760,7 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
   const size_t wb = wbytes(D);
   float* x_out = io.x_out;
   const int32_t* row0_dev = &s->hdr->row0;
-  if (s->tc) {
+  if (s->tc && !fused_prep) {
     // bf16 normed input of layer_a's attention norm + its statistic
     SP_CHECK(launch_pdl(prep_kernel, dim3(n), dim3(256), 0, st, (const float*)x_out, d,
                         s->layers[layer_a - s->lo].attn_norm, s->xb, s->ss,
