@@ -35,7 +35,10 @@ __device__ __forceinline__ void push_top2(LmPartial& s, const Top2& t) {
 
 
 constexpr int LM_ROWS = 8;        // weight rows per block (gemv_core tile)
-constexpr int LM_CTAS = 4 * 148;  // persistent grid: a fixed constant, so the
+#ifndef LM_CTAS_DEF
+#define LM_CTAS_DEF (4 * 148)
+#endif
+constexpr int LM_CTAS = LM_CTAS_DEF;  // persistent grid: a fixed constant, so the
                                   // per-CTA partition (and conf's summation
                                   // order) never depends on the device
 
