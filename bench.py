@@ -243,6 +243,8 @@ def bench_knobs(args) -> dict:
         v = getattr(args, k, None)
         if v is not None:
             kw[k] = v
+    if getattr(args, "no_continuous", False):   # reference knob (engine.py:102)
+        kw["continuous"] = False
     if getattr(args, "no_ramp", False):
         kw["spec_ramp"] = False
     if getattr(args, "free_draft", False):   # experiment only: draft proposals cost nothing
@@ -337,6 +339,7 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
                               os.environ.get("SP_DRAFT_KERNEL", "cluster")
                               if os.environ.get("SP_DRAFT_FUSED", "1") != "0" else "per-forward",
                               "spec_ramp": eng.cfg.spec_ramp,
+                              "continuous": eng.cfg.continuous,
                               **({"free_draft": True} if not eng.cfg.draft_charge else {})},
                    "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
         "itl_ms": round(itl * 1e3, 3),
@@ -397,6 +400,9 @@ def main():
     ap.add_argument("--gen-len", type=int, default=GEN_LEN)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-continuous", action="store_true",
+                    help="engine knob (reference ExperimentConfig.continuous=False): one speculative"
+                         " micro-batch per accepted round")
     ap.add_argument("--no-ramp", action="store_true",
                     help="engine knob: full micro-batches from a fresh chain (spec_ramp=False)")
     ap.add_argument("--free-draft", action="store_true",
