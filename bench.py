@@ -400,6 +400,9 @@ def main():
     ap.add_argument("--gen-len", type=int, default=GEN_LEN)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--node-weights", type=lambda v: tuple(float(x) for x in v.split(",")),
+                    default=None, help="pipeline stage speed weights (reference node_weights,"
+                                       " engine.py:186-224), e.g. 0.8,1")
     ap.add_argument("--no-continuous", action="store_true",
                     help="engine knob (reference ExperimentConfig.continuous=False): one speculative"
                          " micro-batch per accepted round")
