@@ -329,11 +329,12 @@ __device__ void mk_attention(const MkArgs& a, const MkLayer& L, MkSmem* sm, int 
     }
     if (tid == 0) { sp_[0] = mx; sp_[1] = sum; }
     stamp(32);
-    __threadfence();
     epi_sync();
-    if (tid == 0) {
+    if (tid == 0) {   // one fence per CTA: the barrier orders the other threads' stores
+      __threadfence();
       const int t = atomicAdd(&a.att_tickets[(i * a.H + h) * a.att_tstride], 1);
       sm->last = (t == ns - 1);
+      __threadfence();
     }
     epi_sync();
     stamp(33);
@@ -345,7 +346,6 @@ __device__ void mk_attention(const MkArgs& a, const MkLayer& L, MkSmem* sm, int 
       ++unit_k;
     }
     if (sm->last) {
-      __threadfence();
       // all partials of this (query, head) in one coalesced round trip, then
       // the split-order merge from shared memory
       const float* base = a.att_scratch + ((size_t)i * a.H + h) * a.nsplit * (HD + 2);
@@ -608,17 +608,17 @@ stage_mk_kernel(const __grid_constant__ CUtensorMap mXb, const __grid_constant__
 #pragma unroll
                 for (int c = 0; c < MK_NT; ++c)
                   if (c < mv) slot[c * TC_BM + row] = acc[c];
-                __threadfence();
                 epi_sync();
-                if (tid == 0) {
+                if (tid == 0) {   // one fence per CTA: the barrier orders the stores
+                  __threadfence();
                   const int t = atomicAdd(&a.tickets[tile * 16], 1);
                   sm->last = (t == nseg - 1);
+                  __threadfence();
                 }
                 epi_sync();
                 mine = sm->last != 0;
                 if (mine) {
                   ++nmerge;
-                  __threadfence();
                   // K order: segments 0..nseg-1 (own partial from registers);
                   // every peer partial of a token column in flight at once
                   float sum[MK_NT];
