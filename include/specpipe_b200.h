@@ -362,6 +362,13 @@ int sp_stage_error_ptr(sp_stage* s, int** dev_err);
 int sp_stage_plan_sync(sp_stage* s, int32_t* host_vis, int32_t* host_len,
                        int n, void* stream);
 int sp_stage_ld_vis(const sp_stage* s);
+/* eval_layers(..., mask=TreeAttentionMask) (model.py:326-373): install a
+ * caller-built plan -- per query ``host_len[i]`` rows of ``host_vis`` (row
+ * stride sp_stage_ld_vis), cache rows and this batch's rows
+ * (n_cells + j) in gather order, the query's own row last -- for the next
+ * non-continuation forward, which then skips building the plan (K4). */
+int sp_stage_set_plan(sp_stage* s, const int32_t* host_vis, const int32_t* host_len,
+                      int n, void* stream);
 /* K4/K11: build the plan ``host_toks`` would get against the current table
  * (without inserting its cells); visible counts = plan lengths - 1. */
 int sp_stage_plan_only(sp_stage* s, const sp_token* host_toks, int n,

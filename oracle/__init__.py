@@ -7,7 +7,8 @@ path (``paper_2407_11798_b200``), never to *be* it:
 
 * only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
   / ``--impl reference`` legs may import it;
-* the product package never imports it (``tests/test_layering.py`` enforces
+* the product package never imports it
+  (``tests/test_host_cpu.py::test_product_never_imports_oracle`` enforces
   this), and the product fails loudly when its CUDA library is missing.
 
 Parity pinning: the restatement is pinned against golden vectors produced by

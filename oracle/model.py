@@ -182,10 +182,13 @@ def visible_counts(tokens, cache: OracleCache, layer: Optional[int] = None):
 
 def eval_layers(model: OracleModel, lo: int, hi: int,
                 x_in: Optional[np.ndarray], tokens: Sequence,
-                cache: OracleCache) -> np.ndarray:
+                cache: OracleCache, plans: Optional[list] = None) -> np.ndarray:
     """Layers [lo, hi) over a token batch (``model.py:326-421``).
 
     ``tokens``: sequence of (token_id, pos, frozenset(seqs), want_logits).
+    ``plans``: a caller-supplied mask (``model.py:369-373``) as per-query
+    ``[(src, idx)]`` lists (src 0 = raw cache row, 1 = batch index), in
+    gather order; default: derived from cache membership.
     """
     cfg = model.cfg
     if not 0 <= lo < hi <= cfg.n_layers:
@@ -203,7 +206,8 @@ def eval_layers(model: OracleModel, lo: int, hi: int,
         if x_in is None or x_in.shape != (n, d):
             raise OracleModelError("bad input activations")
         x = np.array(x_in, dtype=np.float64)
-    plans = _plans(tokens, cache, lo)
+    if plans is None:
+        plans = _plans(tokens, cache, lo)
     H, hd, KH = cfg.n_heads, cfg.head_dim, cfg.kv_heads
     grp = H // KH
     scale = 1.0 / math.sqrt(hd)

@@ -28,7 +28,10 @@ from .model import (  # noqa: F401
     ModelConfig,
     RowResult,
     SerialDecoder,
+    TreeAttentionMask,
+    build_mask_from_cache,
     build_model,
+    build_tree_mask,
     eval_layers,
     greedy_sample,
     llama_config,
@@ -68,3 +71,20 @@ from .engine import (  # noqa: F401
 LayeredModel = DeviceModel
 
 __version__ = "0.1.0"
+
+# the reference's public names (specpipe/__init__.py:3-58) plus the B200 extras
+__all__ = [
+    "AllocationExhausted", "Batch", "BatchToken", "CutoffController", "ExperimentConfig",
+    "KVCache", "LayeredModel", "ModelConfig", "SequenceAllocator", "SimResult",
+    "SpeculationState", "SyntheticDraft", "ToyDraft", "VerifyResult", "apply_acceptance",
+    "build_model", "build_tree_mask", "detect_stale_runs", "eval_layers", "greedy_sample",
+    "logits", "plan_layer_split", "reference_decode", "rollback_draft", "sample_prompt",
+    "simulate", "speculate_microbatch", "verify_run",
+    # B200 additions
+    "TreeAttentionMask", "build_mask_from_cache", "generate", "RunMetrics", "RunRecord",
+    "token_checksum", "DeviceModel", "SerialDecoder", "RowResult", "max_softmax",
+    "second_best", "llama_config", "free_sequence", "CacheError", "ModelError",
+    "EngineError", "ProtocolError", "SpeculationError", "TransportError", "VerifyError",
+    "LibraryMissing", "DraftBackend", "sync_backend", "NON_SPECULATIVE", "PREFILL",
+    "SPECULATIVE", "VerifyResult",
+]

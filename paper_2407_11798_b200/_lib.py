@@ -126,6 +126,7 @@ PROTOTYPES = {
     "sp_stage_error_ptr": (I, [P, P]),
     "sp_stage_plan_sync": (I, [P, P, P, I, P]),
     "sp_stage_ld_vis": (I, [P]),
+    "sp_stage_set_plan": (I, [P, P, P, I, P]),
     "sp_stage_plan_only": (I, [P, P, I, I, P]),
     "sp_host_register": (I, [P, C.c_size_t, P]),
     "sp_host_unregister": (I, [P]),

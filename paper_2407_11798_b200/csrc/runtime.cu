@@ -351,6 +351,9 @@ struct sp_stage {
   int cur_max_pos = 0;
   int cur_flags = 0;
   bool cur_valid = false;
+  // caller-supplied attention plan (eval_layers(mask=...)): the next
+  // forward uses s->vis/vis_len as uploaded instead of building them
+  bool host_plan = false;
 };
 
 static int cuda_status(cudaError_t e) { return e == cudaSuccess ? SP_OK : SP_ERR_CUDA; }
@@ -734,10 +737,11 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     SP_CHECK(cudaMemcpyAsync(io.x_out, io.x_in, sizeof(float) * (size_t)n * d,
                              cudaMemcpyDeviceToDevice, st));
   }
-  if (!cont)
+  if (!cont && !s->host_plan)
     SP_CHECK(launch_plan(s->cell_pos, s->cell_mask, 0, 0, s->hdr_toks, n, D.max_context,
                          s->vis, s->vis_len, s->ld_vis, 0, s->err, st, s->run_state,
                          s->hdr));
+  if (!cont) s->host_plan = false;
   // launch bound on visible entries per query (+ self): chain batches see
   // exactly pos cells; a graph must hold for any run (context cap)
   const int bound = graphable ? (D.max_context + s->max_tokens)
@@ -1289,6 +1293,29 @@ extern "C" int sp_stage_plan_sync(sp_stage* s, int32_t* host_vis,
 }
 
 extern "C" int sp_stage_ld_vis(const sp_stage* s) { return s ? s->ld_vis : -1; }
+
+extern "C" int sp_stage_set_plan(sp_stage* s, const int32_t* host_vis, const int32_t* host_len,
+                                 int n, void* stream) {
+  // caller-supplied TreeAttentionMask (model.py:369-373): per query, the
+  // rows it attends to in gather order, its own row last; consumed by the
+  // next non-continuation forward of this stage (which skips K4)
+  if (!s || !host_vis || !host_len || n <= 0 || n > s->max_tokens) return SP_ERR_ARG;
+  for (int i = 0; i < n; ++i) {
+    if (host_len[i] < 1 || host_len[i] > s->ld_vis || host_len[i] > s->n_cells + n)
+      return SP_ERR_ARG;
+    for (int j = 0; j < host_len[i]; ++j) {
+      const int r = host_vis[(size_t)i * s->ld_vis + j];
+      if (r < 0 || r >= s->n_cells + n) return SP_ERR_ARG;
+    }
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  SP_CHECK(cudaMemcpyAsync(s->vis, host_vis, 4 * (size_t)n * s->ld_vis, cudaMemcpyHostToDevice,
+                           st));
+  SP_CHECK(cudaMemcpyAsync(s->vis_len, host_len, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  SP_CHECK(cudaStreamSynchronize(st));   // host buffers are the caller's
+  s->host_plan = true;
+  return SP_OK;
+}
 
 extern "C" int sp_embed(const sp_model_dims* dims, const void* emb,
                         const float* pos_table, const sp_token* toks, int n,

@@ -59,6 +59,14 @@ class ControlPlane:
     def __init__(self, name: str, create: bool, n_ranks: int, max_tokens: int,
                  n_stat: int):
         from multiprocessing import shared_memory
+        import platform
+        # Records are published by a plain store of the ring index after the
+        # record bytes, and results are read after their flag: correct under
+        # x86-TSO only (no acquire/release from numpy).  A weakly ordered host
+        # (aarch64 Grace) needs real fences here -- refuse rather than race.
+        if platform.machine() not in ("x86_64", "AMD64"):
+            raise RuntimeError("dist.ControlPlane relies on x86-TSO store ordering; "
+                               f"host is {platform.machine()}")
         self.n_ranks = n_ranks
         self.res_rows = 1 + max_tokens   # [status, err, -, -] + rows
         self.res_bytes = _align(self.res_rows * 16, 256)

@@ -137,6 +137,14 @@ class ExperimentConfig:
             raise EngineError("repetitions must be >= 1")
         if self.prompt_len > self.max_run_tokens:
             raise EngineError("prompt_len exceeds max_run_tokens")
+        # the bounded cell pool must hold the canonical sequence plus one run
+        # per partition after a compaction (kvcache.py grows without bound)
+        need = self.prompt_len + self.gen_len + self.partitions * (
+            max(self.microbatch, self.tree_cap) + 1)
+        if self.capacity < need:
+            raise EngineError(f"capacity {self.capacity} cannot hold a {self.prompt_len}+"
+                              f"{self.gen_len}-token context plus one run per partition "
+                              f"(need >= {need})")
         self.target_config().validate()
         if self.uses_draft():
             self.draft_config().validate()
@@ -888,7 +896,7 @@ class Engine:
                 for st in getattr(self.pipe, "stages", []):
                     if st.device == self.device and st.cfg.arch == "llama":
                         st.set_cta_budget(ctas)
-        self._tables: Dict[int, tuple] = {}
+        self._tables: Dict[tuple, tuple] = {}
 
     def _make_draft(self, prompt: List[int], prompt_seed: int):
         from .drafting import ModelDraftServer, TableDraftServer
@@ -896,8 +904,11 @@ class Engine:
         if not cfg.uses_draft():
             return None
         if cfg.draft_backend == "synthetic":
-            key = hash(tuple(prompt))
-            if key not in self._tables:
+            key = tuple(prompt)
+            need = len(prompt) + min(cfg.gen_len + 16, cfg.max_context - len(prompt) - 1)
+            if key not in self._tables or len(self._tables[key][0]) < need:
+                if len(self._tables) > 64:
+                    self._tables.clear()
                 self._tables[key] = self.truth(prompt, cfg.gen_len + 16)
             truth, runner = self._tables[key]
             seed = cfg.draft_seed * 1000003 + prompt_seed
@@ -981,17 +992,17 @@ class Engine:
 _ENGINES: Dict[tuple, Engine] = {}
 
 
-def simulate(cfg: ExperimentConfig, target_model=None, draft_model=None) -> SimResult:
-    """Run one experiment to completion on the GPU (engine.py:1293-1356).
+def _engine_key(cfg: ExperimentConfig, target_model=None, draft_model=None) -> tuple:
+    """Everything that shapes an Engine's resident state: the models, the
+    stage split, the cell pools and run buffers, the draft's kernel path."""
+    return (cfg.target_config(), cfg.draft_config() if cfg.uses_draft() else None,
+            cfg.n_stages(), cfg.node_weights, cfg.partitions, cfg.capacity,
+            cfg.max_run_tokens, cfg.uses_draft(), cfg.draft_tc, cfg.draft_sm_reserve,
+            id(target_model), id(draft_model))
 
-    Engines (models + stages) are cached per model-shaping config so
-    repeated calls with different seeds/modes reuse resident weights.
-    """
-    cfg.validate()
-    key = (cfg.target_config(), cfg.draft_config() if cfg.uses_draft() else None,
-           cfg.n_stages(), cfg.node_weights, cfg.partitions, cfg.capacity,
-           cfg.max_run_tokens, cfg.mode in ("sync-speculative", "async-speculative"),
-           id(target_model), id(draft_model))
+
+def _engine_for(cfg: ExperimentConfig, target_model=None, draft_model=None) -> "Engine":
+    key = _engine_key(cfg, target_model, draft_model)
     eng = _ENGINES.get(key)
     if eng is None:
         if len(_ENGINES) > 4:
@@ -999,7 +1010,17 @@ def simulate(cfg: ExperimentConfig, target_model=None, draft_model=None) -> SimR
         eng = Engine(cfg, target_model, draft_model)
         _ENGINES[key] = eng
     eng.cfg = cfg
-    return eng.run()
+    return eng
+
+
+def simulate(cfg: ExperimentConfig, target_model=None, draft_model=None) -> SimResult:
+    """Run one experiment to completion on the GPU (engine.py:1293-1356).
+
+    Engines (models + stages) are cached per model-shaping config so
+    repeated calls with different seeds/modes reuse resident weights.
+    """
+    cfg.validate()
+    return _engine_for(cfg, target_model, draft_model).run()
 
 
 def generate(prompt: Sequence[int], cfg: Optional[ExperimentConfig] = None,
@@ -1007,11 +1028,4 @@ def generate(prompt: Sequence[int], cfg: Optional[ExperimentConfig] = None,
     """Greedy generation of ``cfg.gen_len`` tokens after ``prompt``."""
     cfg = replace(cfg or ExperimentConfig(), prompt_len=len(prompt), **overrides)
     cfg.validate()
-    key = ("gen", cfg.target_config(), cfg.draft_config() if cfg.uses_draft() else None,
-           cfg.n_stages(), cfg.mode)
-    eng = _ENGINES.get(key)
-    if eng is None:
-        eng = Engine(cfg)
-        _ENGINES[key] = eng
-    eng.cfg = cfg
-    return eng.run(prompt=list(prompt)).tokens
+    return _engine_for(cfg).run(prompt=list(prompt)).tokens

@@ -533,13 +533,135 @@ def _validate_batch(model: DeviceModel, batch: Batch, lo: int) -> None:
             raise ModelError("negative position")
 
 
+@dataclass
+class TreeAttentionMask:
+    """Per-query visibility (model.py:197-259): which cache cells and which
+    batch tokens each query attends to, in ascending position order.
+
+    ``plans[i] = (sel, cache_rows, batch_rows)``: ``sel`` marks, entry by
+    entry of query i's gather order, whether it is a cache cell (True, the
+    next of ``cache_rows``, raw cell rows) or a batch token (False, the next
+    of ``batch_rows``, indices into the batch); every query also sees itself
+    (appended last, model.py:394-415).  ``order`` is the unmerged form
+    ``[(source, index)]`` (source 0 = cache-view index, 1 = batch index) that
+    ``build_tree_mask`` produces; ``cache_rows`` maps view indices to rows.
+    """
+
+    n_tokens: int
+    n_cells: int
+    order: Optional[list] = None
+    cache_rows: Optional[np.ndarray] = None
+    plans: Optional[list] = None
+
+    def gather_plans(self) -> list:
+        if self.plans is None:
+            out = []
+            for entries in self.order:
+                sel = np.array([src == 0 for src, _ in entries], dtype=bool)
+                crow = np.array([j for src, j in entries if src == 0], dtype=np.int64)
+                if self.cache_rows is not None and crow.size:
+                    crow = np.asarray(self.cache_rows, dtype=np.int64)[crow]
+                brow = np.array([j for src, j in entries if src == 1], dtype=np.int64)
+                out.append((sel, crow, brow))
+            self.plans = out
+        return self.plans
+
+    def visible_counts(self) -> list:
+        return [int(sel.size) for sel, _, _ in self.gather_plans()]
+
+    def cache_matrix(self) -> np.ndarray:
+        m = np.zeros((self.n_tokens, self.n_cells), dtype=bool)
+        if self.order is not None:
+            for i, entries in enumerate(self.order):
+                for src, j in entries:
+                    if src == 0:
+                        m[i, j] = True
+        return m
+
+    def batch_matrix(self) -> np.ndarray:
+        m = np.eye(self.n_tokens, dtype=bool)
+        for i, (_, _, brow) in enumerate(self.gather_plans()):
+            m[i, brow] = True
+        return m
+
+
+def _batch_visibility(tokens, i):
+    q = tokens[i]
+    return [j for j, o in enumerate(tokens)
+            if j != i and o.pos < q.pos and not q.seqs.isdisjoint(o.seqs)]
+
+
+def build_tree_mask(batch: Batch, cache_view: Sequence) -> TreeAttentionMask:
+    """Causal, branch-exclusive mask from a ``(position, sequence_set)`` view
+    of the live cells (model.py:262-284): a query sees an entry iff the
+    entry's position is lower and their sequence sets intersect; entries are
+    merged by position, cache before batch on ties, then by index."""
+    toks = batch.tokens
+    order = []
+    for i, q in enumerate(toks):
+        ent = [(cp, 0, j) for j, (cp, cs) in enumerate(cache_view)
+               if cp < q.pos and not q.seqs.isdisjoint(cs)]
+        ent += [(toks[j].pos, 1, j) for j in _batch_visibility(toks, i)]
+        ent.sort()
+        order.append([(src, j) for _, src, j in ent])
+    return TreeAttentionMask(n_tokens=len(toks), n_cells=len(cache_view), order=order,
+                             cache_rows=getattr(cache_view, "rows", None))
+
+
+def build_mask_from_cache(batch: Batch, cache, layer: Optional[int] = None
+                          ) -> TreeAttentionMask:
+    """The same mask straight off the cache's cell table (model.py:287-323);
+    one table serves every layer of a stage, so ``layer`` is accepted for
+    signature compatibility only."""
+    pos, mask = cache._meta()
+    toks = batch.tokens
+    plans = []
+    for i, q in enumerate(toks):
+        qm = np.uint32(seq_mask(q.seqs))
+        rows = np.where(((mask & qm) != 0) & (pos < q.pos))[0]
+        brow = np.array(_batch_visibility(toks, i), dtype=np.int64)
+        merged = np.concatenate([pos[rows], np.array([toks[j].pos for j in brow],
+                                                     dtype=np.int64)])
+        o = np.argsort(merged, kind="stable")
+        idx = np.concatenate([rows.astype(np.int64), brow])[o]
+        sel = o < rows.size
+        plans.append((sel, idx[sel], idx[~sel]))
+    return TreeAttentionMask(n_tokens=len(toks), n_cells=int(len(pos)), plans=plans)
+
+
+def _plan_rows(mask: TreeAttentionMask, n: int, n_old: int, ld: int):
+    """TreeAttentionMask -> the device plan (rows per query in gather order,
+    own row last; batch token j lives in row n_old + j)."""
+    plans = mask.gather_plans()
+    if len(plans) != n:
+        raise ModelError(f"mask covers {len(plans)} tokens, batch has {n}")
+    vis = np.zeros((n, ld), dtype=np.int32)
+    ln = np.zeros(n, dtype=np.int32)
+    for i, (sel, crow, brow) in enumerate(plans):
+        sel = np.asarray(sel, dtype=bool)
+        if sel.size + 1 > ld:
+            raise ModelError("mask entry list longer than the stage's plan row")
+        row = np.empty(sel.size + 1, dtype=np.int64)
+        row[:-1][sel] = np.asarray(crow, dtype=np.int64)
+        row[:-1][~sel] = n_old + np.asarray(brow, dtype=np.int64)
+        row[-1] = n_old + i
+        if (row[:-1][sel] >= n_old).any() or (row < 0).any():
+            raise ModelError("mask references a cache row that does not exist")
+        vis[i, :row.size] = row
+        ln[i] = row.size
+    return vis, ln
+
+
 def eval_layers(model: DeviceModel, layer_range: tuple, input_acts, batch: Batch,
-                cache, mask=None) -> np.ndarray:
+                cache, mask: Optional[TreeAttentionMask] = None) -> np.ndarray:
     """Evaluate decoder layers ``[lo, hi)`` for a batch (model.py:326-421).
 
     ``cache`` is a ``kvcache.KVCache`` covering (at least) the range; one
     cell per token is appended on its first evaluated range and later
-    sub-ranges of the same batch continue it (split == full).  Returns the
+    sub-ranges of the same batch continue it (split == full).  ``mask``
+    (a ``TreeAttentionMask``) replaces the visibility derived from cache
+    membership, as in the reference (model.py:369-373); its plan is uploaded
+    to the device once and shared by every layer of the range.  Returns the
     float64 host copy of the activations, like the reference.
     """
     import torch
@@ -560,7 +682,10 @@ def eval_layers(model: DeviceModel, layer_range: tuple, input_acts, batch: Batch
     x_in = None
     if lo > 0:
         x_in = torch.as_tensor(np.asarray(input_acts, dtype=np.float32)).to(model.device)
-    x = stage.eval_batch(batch, lo, hi, x_in)
+    plan = None
+    if mask is not None and not stage.continues(batch, lo):
+        plan = _plan_rows(mask, n, stage.n_cells(), stage.ld_vis())
+    x = stage.eval_batch(batch, lo, hi, x_in, plan=plan)
     if not np.all(np.isfinite(x)):
         raise ModelError("non-finite activations")
     return x.astype(np.float64)

@@ -69,6 +69,7 @@ class LocalPipeline:
         self.io = [st.io() for st in self.stages]
         self.capacity = capacity
         self.compactions = 0
+        self._compact_at = 0.75 * capacity
 
     @property
     def n_stages(self) -> int:
@@ -79,6 +80,7 @@ class LocalPipeline:
             raise RuntimeError("reset with runs in flight")
         for st in self.stages:
             st.reset()
+        self._compact_at = 0.75 * self.capacity
         self.cancel_np[:] = 0
         self.stream.synchronize()
 
@@ -94,13 +96,17 @@ class LocalPipeline:
             raise ValueError("a run must request at least one logits row")
         slot = run_id % RESULT_RING
         n = len(toks)
-        if self.stages[0].n_cells() + n > 0.75 * self.capacity:
+        if self.stages[0].n_cells() + n > self._compact_at:
             # bounded cell pool: let the queued runs finish, then reclaim the
             # dead cells (their results stay in the result ring for the head)
             self.stream.synchronize()
+            live = 0
             for st in self.stages:
-                st.compact()
+                live = st.compact()
             self.compactions += 1
+            # a pool that stays mostly live compacts again only when half of
+            # the remaining room is used (never on every launch)
+            self._compact_at = max(0.75 * self.capacity, (live + self.capacity) / 2)
         x_in = stat = None
         last = len(self.stages) - 1
         for i, st in enumerate(self.stages):

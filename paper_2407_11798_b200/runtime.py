@@ -253,13 +253,27 @@ class Stage:
         _lib.raise_device_error(bits, where)
 
     # -- API-mirror conveniences (synchronous) ------------------------------------
-    def eval_batch(self, batch, lo: int, hi: int, x_in) -> np.ndarray:
-        """eval_layers on this stage's cache; continuation of a split range."""
+    def continues(self, batch, lo: int) -> bool:
+        """Is (batch, lo) the next sub-range of the previous eval_batch?"""
+        return batch is self._last_batch and lo == self._last_hi
+
+    def ld_vis(self) -> int:
+        return self.lib.sp_stage_ld_vis(self.h)
+
+    def eval_batch(self, batch, lo: int, hi: int, x_in, plan=None) -> np.ndarray:
+        """eval_layers on this stage's cache; continuation of a split range.
+        ``plan``: (vis, len) rows from a caller's TreeAttentionMask."""
         toks = encode_tokens(batch.tokens)
         n = len(toks)
         if n > self.max_tokens:
             raise CacheError(f"batch of {n} exceeds max_tokens {self.max_tokens}")
-        flags = _lib.SP_FWD_CONTINUE if (batch is self._last_batch and lo == self._last_hi) else 0
+        flags = _lib.SP_FWD_CONTINUE if self.continues(batch, lo) else 0
+        if plan is not None and not flags:
+            vis, ln = plan
+            vis = np.ascontiguousarray(vis, dtype=np.int32)
+            ln = np.ascontiguousarray(ln, dtype=np.int32)
+            check(self.lib.sp_stage_set_plan(self.h, vis.ctypes.data, ln.ctypes.data, n, self.s),
+                  "sp_stage_set_plan")
         if x_in is not None:
             self.xin[:n].copy_(x_in)
         with_stream = self.stream

@@ -237,22 +237,31 @@ def test_stage_compact_moves_live_rows(sp):
 def test_persistent_stage_kernel_streams(sp):
     """The opt-in persistent decode stage (SP_STAGE_MK=1, one launch per
     stage-run, grid barriers between phases, stream-K GEMMs) reproduces the
-    serial greedy stream in every mode (a subprocess: the switch is read once)."""
+    greedy stream of the default kernel chain in every mode.  The expected
+    stream is computed HERE (this process never sets SP_STAGE_MK, so it runs
+    the chain); the subprocess runs everything -- serial decode included --
+    on the persistent kernel and must reproduce it."""
     import os
     import subprocess
     import sys
+    assert os.environ.get("SP_STAGE_MK") in (None, "", "0")
+    c0 = sp.ExperimentConfig(**{**DEEP, "mode": "iterative", "nodes": 1, "gen_len": 24,
+                                "prompt_len": 16, "max_context": 512, "prompt_seed": 5,
+                                "target_seed": 7, "draft_seed": 11})
+    want = sp.reference_decode(c0.target_config(), sp.sample_prompt(5, 16, c0.vocab_size), 24)
     code = (
         "import paper_2407_11798_b200 as sp\n"
         "from paper_2407_11798_b200.engine import ExperimentConfig\n"
         f"base = {DEEP!r}\n"
+        f"want = {want!r}\n"
         "for mode, nodes in [('iterative', 1), ('async-speculative', 4), ('sync-speculative', 3)]:\n"
         "    c = ExperimentConfig(**{**base, 'mode': mode, 'nodes': nodes, 'gen_len': 24,\n"
         "                            'prompt_len': 16, 'max_context': 512, 'prompt_seed': 5,\n"
         "                            'target_seed': 7, 'draft_seed': 11,\n"
         "                            'draft_backend': 'synthetic', 'alpha': 0.5})\n"
         "    res = sp.simulate(c)\n"
-        "    ref = sp.reference_decode(c.target_config(), sp.sample_prompt(5, 16, c.vocab_size), 24)\n"
-        "    assert res.tokens == ref, mode\n"
+        "    assert res.tokens == want, (mode, res.tokens, want)\n"
+        "assert sp.reference_decode(c.target_config(), sp.sample_prompt(5, 16, c.vocab_size), 24) == want\n"
         "print('ok')\n")
     env = dict(os.environ, SP_STAGE_MK="1")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -261,3 +261,44 @@ def test_llama_config_widths_match_oracle(sp, shape, tiled):
         g, o = dec.feed([t]), odec.feed([t])
         errs.append(np.abs(g - o).max())
     assert max(errs) < BF16_TOL, errs
+
+
+def test_eval_layers_honours_caller_mask(sp):
+    """eval_layers(mask=): a caller-built TreeAttentionMask replaces the
+    cache-derived visibility (model.py:369-373).  Golden: the reference run
+    with a build_tree_mask over a view hiding every third cell."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_mask.npz"))
+    cfg = sp.ModelConfig(64, 32, 6, 4, 256, 7)
+    m = sp.build_model(cfg)
+    prompt = [int(t) for t in g["prompt"]]
+    tree = sp.Batch(tokens=tuple(
+        sp.BatchToken(int(t), int(p), frozenset(s for s in range(8) if (int(mk) >> s) & 1), True)
+        for t, p, mk in g["tree"]), kind=sp.SPECULATIVE, run_id=1)
+
+    def fresh():
+        c = sp.KVCache(32, range(6), 256, 8)
+        sp.eval_layers(m, (0, 6), None, _chain(sp, prompt, flag_all=False), c)
+        c.copy(0, [2, 3], len(prompt))
+        return c
+
+    c = fresh()
+    plain = sp.logits(m, sp.eval_layers(m, (0, 6), None, tree, c), tree)
+    assert np.abs(plain - g["plain"]).max() < FP32_TOL
+    c = fresh()
+    derived = sp.build_mask_from_cache(tree, c)
+    again = sp.logits(m, sp.eval_layers(m, (0, 6), None, tree, c, mask=derived), tree)
+    assert np.array_equal(again, plain)          # same plan -> bitwise
+    c = fresh()
+    view = c.snapshot()
+    keep = [i for i in range(len(view)) if i % 3 != 1]
+    from paper_2407_11798_b200.kvcache import CacheView
+    sub = CacheView([view[i] for i in keep], np.asarray(view.rows)[keep])
+    mask = sp.build_tree_mask(tree, sub)
+    custom = sp.logits(m, sp.eval_layers(m, (0, 6), None, tree, c, mask=mask), tree)
+    assert np.abs(custom - g["custom"]).max() < FP32_TOL
+    # split evaluation under a caller mask continues the same plan
+    c = fresh()
+    x = sp.eval_layers(m, (0, 2), None, tree, c, mask=mask)
+    x = sp.eval_layers(m, (2, 6), x, tree, c, mask=mask)
+    assert np.array_equal(sp.logits(m, x, tree), custom)

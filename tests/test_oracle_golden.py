@@ -177,3 +177,26 @@ def test_allocator_sequence(golden):
             assert a.alloc() == s
         else:
             a.free(s)
+
+
+def test_oracle_caller_mask_matches_reference():
+    """eval_layers(..., mask=) -- a caller-built mask that hides cache cells
+    (reference model.py:369-373, golden from make_mask_golden.py)."""
+    import os
+    from oracle import model as OM
+    from oracle.kvcache import OracleCache
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_mask.npz"))
+    m = OM.build_ref_model(OM.OracleConfig(64, 32, 6, 4, 256, 7))
+    prompt = [int(t) for t in g["prompt"]]
+    toks = [(int(t), int(p), frozenset(s for s in range(8) if (int(mk) >> s) & 1), True)
+            for t, p, mk in g["tree"]]
+    plans = [[] for _ in toks]
+    for i, src, j in g["order"]:
+        plans[int(i)].append((int(src), int(j)))
+    for use_mask, want in ((False, g["plain"]), (True, g["custom"])):
+        c = OracleCache(32, range(6), 256, 8)
+        OM.eval_layers(m, 0, 6, None, [(t, i, frozenset([0]), False)
+                                       for i, t in enumerate(prompt)], c)
+        c.copy(0, [2, 3], len(prompt))
+        x = OM.eval_layers(m, 0, 6, None, toks, c, plans=plans if use_mask else None)
+        assert np.array_equal(OM.logits(m, x, toks), want)
