@@ -320,6 +320,9 @@ int sp_stage_io(sp_stage* s, float** x_out, sp_row_result** res);
  * layer + head, one sequence, rows == positions (pos0 == n_cells; see
  * sp_stage_truncate).  Appends n_feed + steps cells.  Replaces the draft
  * node's per-token loop (engine.py:640-688, speculation.py:142-195). */
+/* 1 if this stage's shape runs on the persistent draft kernels (else the
+ * caller uses one sp_stage_step per forward). */
+int sp_stage_decode_chain_ok(const sp_stage* s);
 int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_feed, int pos0,
                           const int32_t* step_tokens, int steps, float cutoff,
                           sp_row_result* out, int* err_out, void* stream);

@@ -109,6 +109,7 @@ PROTOTYPES = {
     "sp_stage_io": (I, [P, P, P]),
     "sp_stage_decode_chain": (I, [P, P, I, I, P, I, F, P, P, P]),
     "sp_stage_truncate": (I, [P, I]),
+    "sp_stage_decode_chain_ok": (I, [P]),
     "sp_stage_compact": (I, [P, P]),
     "sp_stage_draft_profile": (I, [P, P, I]),
     "sp_stage_chain_begin": (I, [P, F, P, P]),

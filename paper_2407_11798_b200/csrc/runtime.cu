@@ -1420,6 +1420,26 @@ extern "C" int sp_stage_truncate(sp_stage* s, int n_cells) {
   return SP_OK;
 }
 
+// Shapes the persistent draft kernels (draft.cu / draft2.cu) take: a whole
+// llama bf16 model with row-major SWZ8 weights, head dim 64/128, and widths
+// whose per-CTA slices fit the shared-memory plan (the 160M draft does;
+// TinyLlama's ffn 5632 does not -- it runs the per-forward path).
+static bool decode_chain_shape_ok(const sp_stage* s) {
+  const sp_model_dims& D = s->dims;
+  if (D.arch != SP_ARCH_LLAMA || D.w_dtype != SP_DTYPE_BF16 || !s->swz || s->lo != 0 ||
+      s->hi != D.n_layers || !s->emb || !s->w_out || !s->final_norm || s->n_seq != 1 ||
+      (D.head_dim != 64 && D.head_dim != 128) || D.d_model % 8 || D.ffn_dim % 8 ||
+      D.d_model > 2048 || D.ffn_dim > 4096 || D.n_layers > DR_MAX_LAYERS)
+    return false;
+  for (const LayerW& L : s->layers)
+    if (!L.qkv || !L.attn_norm || !L.mlp_norm) return false;
+  return true;
+}
+
+extern "C" int sp_stage_decode_chain_ok(const sp_stage* s) {
+  return s && decode_chain_shape_ok(s) ? 1 : 0;
+}
+
 extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_feed, int pos0,
                                      const int32_t* step_tokens, int steps, float cutoff,
                                      sp_row_result* out, int* err_out, void* stream) {
@@ -1427,13 +1447,7 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
       (n_feed > 0 && !feed))
     return SP_ERR_ARG;
   const sp_model_dims& D = s->dims;
-  if (D.arch != SP_ARCH_LLAMA || D.w_dtype != SP_DTYPE_BF16 || !s->swz || s->lo != 0 ||
-      s->hi != D.n_layers || !s->emb || !s->w_out || !s->final_norm || s->n_seq != 1 ||
-      (D.head_dim != 64 && D.head_dim != 128) || D.d_model % 8 || D.ffn_dim % 8 ||
-      D.d_model > 2048 || D.ffn_dim > 4096 || D.n_layers > DR_MAX_LAYERS)
-    return SP_ERR_ARG;
-  for (const LayerW& L : s->layers)
-    if (!L.qkv || !L.attn_norm || !L.mlp_norm) return SP_ERR_ARG;
+  if (!decode_chain_shape_ok(s)) return SP_ERR_ARG;
   if (pos0 != s->n_cells) return SP_ERR_PROTOCOL;   // rows == positions
   const int total = n_feed + steps;
   if (s->n_cells + total > s->cap || pos0 + total > D.max_context) return SP_ERR_CAPACITY;

@@ -236,6 +236,13 @@ class _StageRank:
                 check(self.stage.lib.sp_signal(self.plane.flag_dev(slot), run_id, s))
         self._reap()
 
+    def finish(self) -> None:
+        import torch
+        self.stream.synchronize()
+        while self.works:
+            self.works.popleft().wait()
+        torch.cuda.synchronize()
+
     def copy(self, src, dst_mask, end) -> None:
         dsts = [i for i in range(32) if (dst_mask >> i) & 1]
         self.stage.cache_copy(src, dsts, end)
@@ -245,10 +252,13 @@ class _StageRank:
 
 
 def worker_loop(model, lo, hi, rank, world, plane: ControlPlane, partitions,
-                capacity, max_tokens, on_mark=None, first: int = 0) -> None:
-    """Ranks >= 1: serve control records until SHUTDOWN (never blocks on the GPU)."""
-    import torch
-    sr = _StageRank(model, lo, hi, rank, world, plane, partitions, capacity, max_tokens, first)
+                capacity, max_tokens, on_mark=None, first: int = 0,
+                stage_rank=None) -> None:
+    """Ranks >= 1: serve control records until SHUTDOWN (never blocks on the GPU).
+    ``stage_rank`` replaces the GPU stage (``_StageRank``) -- CPU control-plane
+    tests only."""
+    sr = (stage_rank or _StageRank)(model, lo, hi, rank, world, plane, partitions, capacity,
+                                    max_tokens, first)
     while True:
         rtype, p = plane.read(rank)
         if rtype == R_RUN:
@@ -268,10 +278,7 @@ def worker_loop(model, lo, hi, rank, world, plane: ControlPlane, partitions,
             if on_mark is not None:
                 on_mark(struct.unpack("<i", p[:4])[0], sr.stage.launches)
         elif rtype == R_SHUTDOWN:
-            sr.stream.synchronize()
-            while sr.works:
-                sr.works.popleft().wait()
-            torch.cuda.synchronize()
+            sr.finish()
             return
 
 
@@ -279,7 +286,7 @@ class DistPipeline:
     """Head-side pipeline over torchrun ranks (rank 0 = head + stage 0)."""
 
     def __init__(self, model, ranges, plane: ControlPlane, world: int, partitions=8,
-                 capacity=8192, max_tokens=256, local_stage: bool = True):
+                 capacity=8192, max_tokens=256, local_stage: bool = True, stage_rank=None):
         """``local_stage``: rank 0 hosts stage 0 (and the draft shares its
         GPU); False: rank 0 is the head + dedicated draft node and the
         stages live on ranks 1.. (the reference's n_stages = nodes - 1 with a
@@ -294,8 +301,8 @@ class DistPipeline:
         self.stages = []
         if local_stage:
             lo, hi = ranges[0]
-            self.sr = _StageRank(model, lo, hi, 0, world, plane, partitions, capacity,
-                                 max_tokens)
+            self.sr = (stage_rank or _StageRank)(model, lo, hi, 0, world, plane, partitions,
+                                                 capacity, max_tokens)
             self.stages = [self.sr.stage]
         self.fifo: deque = deque()
         self.n_stat = (world + 3) // 4

@@ -56,10 +56,7 @@ class _DraftBase:
         self.res_host = torch.zeros((8, 2, 4), dtype=torch.int32).pin_memory()
         self._blocks: List[int] = []
         cfgm = draft_model.config
-        self.fused_ok = (cfgm.arch == "llama" and cfgm.weight_dtype != "fp32"
-                         and not getattr(draft_model, "tiled", True)
-                         and getattr(draft_model, "swz", False)
-                         and cfgm.head_dim in (64, 128))
+        self.fused_ok = bool(self.stage.lib.sp_stage_decode_chain_ok(self.stage.h))
         # one persistent launch per request (K15): the cluster form (16 SMs)
         # by default, the grid form (every SM) on a dedicated draft GPU;
         # SP_DRAFT_FUSED=0 falls back to one graph-replayed step per forward

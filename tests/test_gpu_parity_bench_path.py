@@ -67,9 +67,12 @@ def test_headline_widths_match_oracle(sp, shape, tiled, layers):
     assert max(errs) < BF16_TOL, errs
 
 
-def _draft_vs_oracle(sp, kernel, shape_kw, n_req=8, budget=4, seed=2):
-    """Drive a fused ModelDraftServer with ``SP_DRAFT_KERNEL=kernel`` and check
-    each chained proposal against the oracle's step on the same context."""
+def _draft_vs_oracle(sp, kernel, shape_kw, n_req=8, budget=4, seed=2, fused=True):
+    """Drive a ModelDraftServer with ``SP_DRAFT_KERNEL=kernel`` and check each
+    chained proposal against the oracle's step on the same context.  ``fused``
+    says which path the shape takes: the persistent kernels, or (widths past
+    their shared-memory plan, sp_stage_decode_chain_ok == 0) one graph-replayed
+    stage step per forward."""
     import torch
     from paper_2407_11798_b200.drafting import ModelDraftServer
     old = os.environ.get("SP_DRAFT_KERNEL")
@@ -78,7 +81,7 @@ def _draft_vs_oracle(sp, kernel, shape_kw, n_req=8, budget=4, seed=2):
         cfg = sp.ModelConfig(**shape_kw)
         m = sp.build_model(cfg, torch.device("cuda", 0), tiled=False)
         srv = ModelDraftServer(m, capacity=1024)
-        assert srv.fused, "the persistent draft kernel must be the path under test"
+        assert srv.fused == fused, "the path under test must be the one the product takes"
         OM, om = _oracle_for(sp, m, cfg)
         rng = np.random.default_rng(seed)
         prompt = rng.integers(0, cfg.vocab_size, 12).tolist()
@@ -131,9 +134,15 @@ DRAFT_SHAPES = {
 
 
 @pytest.mark.parametrize("kernel", ["cluster", "grid"])
-@pytest.mark.parametrize("shape", list(DRAFT_SHAPES))
-def test_persistent_draft_kernels_match_oracle(sp, kernel, shape):
-    _draft_vs_oracle(sp, kernel, DRAFT_SHAPES[shape])
+def test_persistent_draft_kernels_match_oracle(sp, kernel):
+    _draft_vs_oracle(sp, kernel, DRAFT_SHAPES["160m"])
+
+
+def test_per_forward_draft_1b_matches_oracle(sp):
+    """TinyLlama-1.1B widths (configs[2]/[3]'s draft): ffn 5632 exceeds the
+    persistent kernels' per-CTA slice plan, so the product drafts with one
+    stage step per forward; same oracle check."""
+    _draft_vs_oracle(sp, "cluster", DRAFT_SHAPES["1.1b"], fused=False)
 
 
 def test_synthetic_emissions_match_reference(sp, golden):
