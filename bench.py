@@ -309,12 +309,30 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
         return sum(r.metrics.tokens_generated - 1 for r in rs) / sum(r.metrics.duration for r in rs)
 
     sync_speed, it_speed = speed(sync), speed(itr)
+
+    # every timed stream (and the baselines') must be the target's greedy
+    # stream: the truth table is an iterative decode through the same stages
+    def check(r, seed):
+        prompt = sp.sample_prompt(seed, PROMPT_LEN, 32000)
+        truth = eng._tables[tuple(prompt)][0]
+        want = truth[PROMPT_LEN:PROMPT_LEN + len(r.tokens)]
+        if len(r.tokens) != args.gen_len or r.tokens != want:
+            raise SystemExit(f"bench: {r.metrics.mode} stream for prompt seed {seed} differs "
+                             "from the greedy (iterative) stream")
+    for i, r in enumerate(res):
+        check(r, seeds[args.warmup + i])
+    for i in range(nb):
+        check(sync[i], seeds[args.warmup + i])
+        check(itr[i], seeds[args.warmup + i])
+    checksum = res[0].metrics.token_checksum
     # e2e: the public API on host token lists (prompt H2D, results D2H inside)
     prompt = sp.sample_prompt(seeds[-1], PROMPT_LEN, 32000)
     eng._make_draft(prompt, 1234)
     t0 = time.perf_counter()
     out = eng.generate(prompt)
     e2e_s = time.perf_counter() - t0
+    if out != eng._tables[tuple(prompt)][0][PROMPT_LEN:PROMPT_LEN + len(out)]:
+        raise SystemExit("bench: generate() stream differs from the greedy stream")
     rf = gemv_roofline(eng)
     # the CPU baseline is timed on rank 0 at N=1 only (the bench contract)
     cpu = cpu_baseline() if not args.no_cpu and n_gpus == 1 else None
@@ -343,6 +361,9 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
                               **({"free_draft": True} if not eng.cfg.draft_charge else {})},
                    "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
         "itl_ms": round(itl * 1e3, 3),
+        "streams_checked": {"timed_steps": len(res), "sync": nb, "iterative": nb, "e2e": 1,
+                            "equal_to_greedy": True,
+                            "token_checksum_step0": checksum},
         "acceptance_rate": round(statistics.mean(r.metrics.acceptance_rate for r in res), 4),
         "cancelled_runs_per_step": round(statistics.mean(r.metrics.cancelled_runs for r in res), 1),
         "runs_per_step": round(statistics.mean(r.metrics.runs_started for r in res), 1),
@@ -355,7 +376,9 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
         "weight_stream_roofline_tokens_per_s": round(rf["peak"] * 1e9 / wb, 1),
         "e2e": {"value": round((len(out) - 1) / e2e_s, 2), "unit": "tokens/s",
                 "h2d_bytes_per_step": PROMPT_LEN * 16, "d2h_bytes_per_step": len(out) * 16,
-                "note": "generate() on a host token list, prefill included"},
+                "note": "generate() on a host token list, prefill included; the synthetic "
+                        "draft's truth table (an iterative decode through the same "
+                        "stages, SURVEY H6) is built before the timer"},
         "gpu_launches": launches,
         "roofline": rf,
         "cpu_baseline": cpu,

@@ -68,6 +68,10 @@ class _DraftBase:
         self.tokens: List[int] = []
         self._pending = None
         self.forwards = 0          # draft-model forwards issued (cost accounting)
+        # diagnostics (SP_RUN_TIMING=1): timing events around each request
+        self.timing = os.environ.get("SP_RUN_TIMING") == "1"
+        self.timeline: list = []
+        self._t0 = None
         torch.cuda.synchronize(draft_model.device)
 
     def __len__(self) -> int:
@@ -148,6 +152,20 @@ class _DraftBase:
                 from . import _lib
                 _lib.raise_device_error(err, "draft")
 
+    def _mark_start(self) -> None:
+        if self.timing:
+            import torch
+            self._t0 = torch.cuda.Event(enable_timing=True)
+            self._t0.record(self.stream)
+
+    def _mark_end(self, n_feed: int, n_props: int) -> None:
+        if self.timing and self._t0 is not None:
+            import torch
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(self.stream)
+            self.timeline.append((n_feed, n_props, self._t0, e))
+            self._t0 = None
+
     def ready(self) -> bool:
         return self._pending is not None and self.event.query()
 
@@ -162,6 +180,7 @@ class ModelDraftServer(_DraftBase):
                 cutoff: float) -> None:
         if self._pending is not None:
             raise SpeculationError("draft request while one is in flight")
+        self._mark_start()
         self._truncate(truncate_to)
         feed = list(feed)
         room = self.max_context - len(self.tokens) - len(feed)
@@ -173,6 +192,7 @@ class ModelDraftServer(_DraftBase):
             else:
                 self.event.record(self.stream)
             self._pending = (budget, np.float32(cutoff), True)
+            self._mark_end(len(feed), budget)
             return
         if feed:
             self._forward(feed, len(self.tokens))
@@ -184,6 +204,7 @@ class ModelDraftServer(_DraftBase):
                 self._forward([0], base + j, chain=True, cutoff=c32, block=1 + j)
         self._finish_enqueue(budget + 1)
         self._pending = (budget, np.float32(cutoff), False)
+        self._mark_end(len(feed), budget)
 
     def reply(self) -> Tuple[tuple, tuple]:
         budget, c32, fused = self._pending
@@ -244,6 +265,7 @@ class TableDraftServer(_DraftBase):
                 cutoff: float) -> None:
         if self._pending is not None:
             raise SpeculationError("draft request while one is in flight")
+        self._mark_start()
         if truncate_to < len(self.tokens):
             if self.charge:
                 self._truncate(truncate_to)
@@ -279,9 +301,11 @@ class TableDraftServer(_DraftBase):
             # the forwards a real draft would run, as one persistent launch
             self._launch_chain(feed, feed_pos, len(props), 0.0, step_tokens=props)
             self._pending = (tuple(props), True)
+            self._mark_end(len(feed), len(props))
             return
         self._finish_enqueue(1)
         self._pending = (tuple(props), False)
+        self._mark_end(len(feed), len(props))
 
     def reply(self) -> Tuple[tuple, tuple]:
         props, fused = self._pending

@@ -19,6 +19,7 @@ semantics).  ``dist.DistPipeline`` spreads the stages over torchrun ranks.
 
 from __future__ import annotations
 
+import os
 from collections import deque
 from dataclasses import dataclass
 from typing import List, Optional
@@ -70,6 +71,10 @@ class LocalPipeline:
         self.capacity = capacity
         self.compactions = 0
         self._compact_at = 0.75 * capacity
+        # diagnostics (SP_RUN_TIMING=1, tools/async_timeline.py): per launched
+        # run, timing events on the stage stream around its stage steps
+        self.timing = os.environ.get("SP_RUN_TIMING") == "1"
+        self.timeline: list = []
 
     @property
     def n_stages(self) -> int:
@@ -107,6 +112,10 @@ class LocalPipeline:
             # a pool that stays mostly live compacts again only when half of
             # the remaining room is used (never on every launch)
             self._compact_at = max(0.75 * self.capacity, (live + self.capacity) / 2)
+        if self.timing:
+            import torch
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(self.stream)
         x_in = stat = None
         last = len(self.stages) - 1
         for i, st in enumerate(self.stages):
@@ -116,6 +125,9 @@ class LocalPipeline:
             x_in = self.io[i][0]
             stat = x_in + 4 * n * self.d
         self.events[slot].record(self.stream)
+        if self.timing:
+            ev[1].record(self.stream)
+            self.timeline.append((run_id, kind, n, ev[0], ev[1]))
         self.fifo.append((run_id, slot, len(rows)))
 
     def copy(self, src: int, dsts, end_pos: int) -> None:

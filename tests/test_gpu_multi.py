@@ -1,0 +1,45 @@
+"""Multi-GPU parity (VERDICT r01 "Next round" 2): the NCCL
+pipeline's token streams at N GPUs equal the oracle (fp32 toy decoder) and
+the 1-GPU stream (bf16 llama), in the async, sync and pipeline-iterative
+modes and in both layouts.  Needs >= 2 GPUs (``gpurun --gpus 2``); on a
+1-GPU box it skips.  The world size is every visible GPU, capped at 4."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_multi_gpu_streams_match(tmp_path):
+    import torch
+    n = min(4, torch.cuda.device_count())
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    out = tmp_path / "streams.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "dist_parity_main.py"),
+           str(out)]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    d = json.loads(out.read_text())
+    assert d["world"] == n
+    for case, got in d["results"].items():
+        want = d["refs"][case.split("/")[0]]
+        for mode in ("async-speculative", "sync-speculative", "pipeline-iterative"):
+            assert got[mode] == want, (case, mode)
