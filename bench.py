@@ -249,6 +249,12 @@ def bench_knobs(args) -> dict:
         kw["spec_ramp"] = False
     if getattr(args, "free_draft", False):   # experiment only: draft proposals cost nothing
         kw["draft_charge"] = False
+    if getattr(args, "reference_policy", False):   # the reference head, unchanged
+        kw.update(fold_frontier=False, max_inflight=0, draft_exclusive=False)
+    if getattr(args, "max_inflight", None) is not None:
+        kw["max_inflight"] = args.max_inflight
+    if getattr(args, "fold", None) is not None:
+        kw["fold_frontier"] = args.fold == "on"
     return kw
 
 
@@ -358,6 +364,13 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
                               if os.environ.get("SP_DRAFT_FUSED", "1") != "0" else "per-forward",
                               "spec_ramp": eng.cfg.spec_ramp,
                               "continuous": eng.cfg.continuous,
+                              "fold_frontier": (eng.pipe.n_stages == 1
+                                                if eng.cfg.fold_frontier is None
+                                                else eng.cfg.fold_frontier),
+                              "max_inflight": ((1 if eng.pipe.n_stages == 1 else 0)
+                                               if eng.cfg.max_inflight is None
+                                               else eng.cfg.max_inflight),
+                              "draft_exclusive": eng.cfg.draft_exclusive,
                               **({"free_draft": True} if not eng.cfg.draft_charge else {})},
                    "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
         "itl_ms": round(itl * 1e3, 3),
@@ -433,6 +446,11 @@ def main():
                     help="engine knob: full micro-batches from a fresh chain (spec_ramp=False)")
     ap.add_argument("--free-draft", action="store_true",
                     help="experiment only (not a headline): the synthetic draft skips its forward")
+    ap.add_argument("--reference-policy", action="store_true",
+                    help="the reference head's scheduling (no frontier folding, unbounded "
+                         "in-flight speculation, draft always on the 16-SM cluster kernel)")
+    ap.add_argument("--max-inflight", type=int, default=None)
+    ap.add_argument("--fold", choices=["on", "off"], default=None)
     ap.add_argument("--microbatch", type=int, default=None)
     ap.add_argument("--partitions", type=int, default=None)
     ap.add_argument("--cutoff", type=float, default=None)

@@ -323,6 +323,15 @@ int sp_stage_io(sp_stage* s, float** x_out, sp_row_result** res);
 /* 1 if this stage's shape runs on the persistent draft kernels (else the
  * caller uses one sp_stage_step per forward). */
 int sp_stage_decode_chain_ok(const sp_stage* s);
+/* Which persistent draft kernel sp_stage_decode_chain launches: the cluster
+ * form (16 SMs; leaves the rest of the GPU to a co-resident target stage) or
+ * the grid form (every SM; for a draft whose GPU is otherwise idle -- a
+ * dedicated draft GPU, or a shared one while no target run is queued).
+ * AUTO follows the SP_DRAFT_KERNEL environment variable (cluster default). */
+#define SP_DRAFT_KIND_AUTO 0
+#define SP_DRAFT_KIND_CLUSTER 1
+#define SP_DRAFT_KIND_GRID 2
+int sp_stage_set_draft_kernel(sp_stage* s, int kind);
 int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_feed, int pos0,
                           const int32_t* step_tokens, int steps, float cutoff,
                           sp_row_result* out, int* err_out, void* stream);

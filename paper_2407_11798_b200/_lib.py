@@ -28,6 +28,7 @@ SP_STATUS_VALID, SP_STATUS_PLACEHOLDER = 0, 1
 SP_FWD_CHECK_COVERAGE, SP_FWD_SKIPPABLE, SP_FWD_CONTINUE, SP_FWD_CHAIN = 1, 2, 4, 8
 SP_EPI_STORE, SP_EPI_RESID, SP_EPI_QKV, SP_EPI_GELU, SP_EPI_SWIGLU = range(5)
 SP_STEP_TIP, SP_STEP_CHAIN = 1, 2
+SP_DRAFT_KIND_AUTO, SP_DRAFT_KIND_CLUSTER, SP_DRAFT_KIND_GRID = 0, 1, 2
 SP_LAYOUT_NATURAL, SP_LAYOUT_TC_TILED, SP_LAYOUT_SWZ8 = 0, 1, 2
 
 
@@ -110,6 +111,7 @@ PROTOTYPES = {
     "sp_stage_decode_chain": (I, [P, P, I, I, P, I, F, P, P, P]),
     "sp_stage_truncate": (I, [P, I]),
     "sp_stage_decode_chain_ok": (I, [P]),
+    "sp_stage_set_draft_kernel": (I, [P, I]),
     "sp_stage_compact": (I, [P, P]),
     "sp_stage_draft_profile": (I, [P, P, I]),
     "sp_stage_chain_begin": (I, [P, F, P, P]),

@@ -9,6 +9,11 @@ namespace sp {
 
 typedef sp_tc_args TcArgs;
 
+// a stage's tensor-core GEMM scratch (split-K partials) and tile tickets;
+// launchers that pass TcArgs::scratch / tickets provide at least this much
+static constexpr int TC_SCRATCH_FLOATS = 8 << 20;
+static constexpr int TC_TICKETS = 4096;
+
 // Per-run scalars read by the kernels of a stage-run (one small H2D copy per
 // run); followed in memory by int32 rows[max_tokens] and sp_token
 // toks[max_tokens].  Keeping them out of kernel arguments makes a stage-run

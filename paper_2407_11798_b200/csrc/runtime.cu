@@ -241,8 +241,6 @@ struct LayerW {
   const float* mlp_norm = nullptr;
 };
 
-static constexpr int TC_SCRATCH_FLOATS = 8 << 20;
-static constexpr int TC_TICKETS = 4096;
 // layers between cancel observations / per conditional graph node (each
 // observation and IF node breaks the PDL chain: 7B stage-run 2.64 ms at 4/8,
 // 2.60 ms at 8/16, and a run cancelled 1 ms in still ends 0.3 ms later)
@@ -329,6 +327,7 @@ struct sp_stage {
   unsigned* dbar = nullptr;
   int draft_ctas = 0;
   int draft_cluster = 0;
+  int draft_kernel = 0;   // SP_DRAFT_KIND_*: 0 = SP_DRAFT_KERNEL env (cluster default)
   int draft_stages = 0;
   long long* dprof = nullptr;            // SP_DRAFT_PROF: phase timestamps
   float* dxb = nullptr;
@@ -1540,7 +1539,9 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
   }
   a.spin_ns = getenv("SP_DRAFT_SPIN_NS") ? (unsigned)atoi(getenv("SP_DRAFT_SPIN_NS")) : 32u;
   const char* kind = getenv("SP_DRAFT_KERNEL");
-  if (kind && std::strcmp(kind, "grid") == 0) {
+  const bool grid = s->draft_kernel == SP_DRAFT_KIND_GRID ||
+                    (s->draft_kernel == SP_DRAFT_KIND_AUTO && kind && std::strcmp(kind, "grid") == 0);
+  if (grid) {
     if (s->draft_ctas <= 0) {
       int dev = 0, sms = 0;
       cudaGetDevice(&dev);
@@ -1589,6 +1590,12 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
   }
   s->n_cells += total;
   s->cur_valid = false;
+  return SP_OK;
+}
+
+extern "C" int sp_stage_set_draft_kernel(sp_stage* s, int kind) {
+  if (!s || kind < SP_DRAFT_KIND_AUTO || kind > SP_DRAFT_KIND_GRID) return SP_ERR_ARG;
+  s->draft_kernel = kind;
   return SP_OK;
 }
 

@@ -111,7 +111,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
   const uint32_t tmem = tail->tmem_base;
   // push merge: publish the initialised reduction barrier to the cluster
   // now, wait for the peers' arrivals only when the partials are ready
-  if (push) cluster_arrive();
+  if (push == 1) cluster_arrive();
 
   // ---- programmatic dependency: everything below may read the previous
   // kernel's outputs (activations, run_state, norm statistics)
@@ -138,7 +138,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
   const int row = warp * 32 + lane;          // row within the tile
   const int R = tile * TC_BM + row;          // global weight row
   const int mv = min(NT, a.m - a.tok0);
-  const bool head = !push || split == 0;     // the CTA that runs the epilogue
+  // the CTA that runs the epilogue (ticket merge: whichever split arrives
+  // last, so every split loads the epilogue operands)
+  const bool head = push != 1 || split == 0;
   if (NORM && head && threadIdx.x >= 64) {   // warps 2-3: not the producer / MMA lanes
     for (int c = threadIdx.x - 64; c < mv; c += 64) {
       float ssum = 0.f;
@@ -223,7 +225,36 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
 
-  if (push) {
+  if (push == 2) {
+    // split-K merge through L2 (no cluster): each split parks its partial in
+    // global scratch; the last to take the tile's ticket sums them in split
+    // order from split 0 -- the same fp32 add sequence as the cluster merges,
+    // so the bits do not depend on the merge path.  Used when a co-resident
+    // draft cluster holds SMs of one GPC: clusters of split CTAs would no
+    // longer all fit in one wave (measured: O / down 2x slower).
+    if (nsplit > 1) {
+      float* part = a.scratch + ((size_t)tile * nsplit + split) * (NT * TC_BM);
+#pragma unroll
+      for (int c = 0; c < NT; ++c)
+        if (c < mv) part[c * TC_BM + row] = acc[c];
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) tail->last = atomicAdd(a.tickets + tile, 1) == nsplit - 1;
+      __syncthreads();
+      if (!tail->last) return;
+      __threadfence();
+      const float* p0 = a.scratch + (size_t)tile * nsplit * (NT * TC_BM);
+#pragma unroll
+      for (int c = 0; c < NT; ++c)
+        if (c < mv) acc[c] = __ldcg(p0 + c * TC_BM + row);
+      for (int sp2 = 1; sp2 < nsplit; ++sp2) {
+#pragma unroll
+        for (int c = 0; c < NT; ++c)
+          if (c < mv) acc[c] = __fadd_rn(acc[c], __ldcg(p0 + ((size_t)sp2 * NT + c) * TC_BM + row));
+      }
+      if (threadIdx.x == 0) a.tickets[tile] = 0;   // the next launch reuses it
+    }
+  } else if (push) {
     // split-K merge by push: the split CTAs of this row tile form one
     // cluster; each peer stores its partial rows straight into rank 0's
     // reduction buffer (st.async, completing on rank 0's barrier) and
@@ -418,8 +449,18 @@ static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
   const int mvl = a.m - a.tok0 < NT ? a.m - a.tok0 : NT;   // token columns of this tile
   const int red = NT == 16 && ksplit > 1 ? (ksplit - 1) * mvl * TC_BM * 4 : 0;
   static const bool nopush = getenv("SP_TC_PULL") != nullptr;   // experiments
-  const int push = red > 0 && !nopush && base + red <= 227 * 1024 ? 1 : 0;
-  const int smem = base + (push ? red : 0);
+  // opt-in (SP_TC_TICKET_MERGE=1, with a sharing budget): merge decode
+  // splits through L2 instead of a cluster (see the kernel).  Measured on
+  // the 7B stage: no slowdown beside a running draft cluster (3.18 vs 3.45
+  // ms) but +0.35-0.55 ms per run without one, so the cluster merge stays
+  // the default and the head keeps the draft off the GPU's SMs instead
+  static const bool tk_merge = getenv("SP_TC_TICKET_MERGE") != nullptr;
+  const bool ticket = NT == 16 && ksplit > 1 && a.max_ctas > 0 && a.max_ctas < 296 &&
+                      tk_merge && a.scratch && a.tickets &&
+                      (size_t)(a.n_rows / TC_BM) * ksplit * NT * TC_BM <= (size_t)TC_SCRATCH_FLOATS &&
+                      a.n_rows / TC_BM <= TC_TICKETS;
+  const int push = ticket ? 2 : red > 0 && !nopush && base + red <= 227 * 1024 ? 1 : 0;
+  const int smem = base + (push == 1 ? red : 0);
   static int configured = 0;
   if (configured < smem) {
     cudaFuncSetAttribute(tc_gemm_kernel<NT, EPI, NORM, ST>,
@@ -437,7 +478,7 @@ static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   attr[1].id = cudaLaunchAttributeClusterDimension;   // the split-K CTAs of a tile
   attr[1].val.clusterDim.x = 1;
-  attr[1].val.clusterDim.y = ksplit;
+  attr[1].val.clusterDim.y = push == 2 ? 1 : ksplit;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
@@ -518,6 +559,8 @@ cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st) 
     // one CTA per SM with a deep ring: split so the grid still fits one wave
     ksplit = a.ksplit > 0 ? a.ksplit
                           : max(1, min(min(sms / tiles, nchunk / 16), 8));
+    static const int ks_cap = getenv("SP_TC_DEEP_KS_MAX") ? atoi(getenv("SP_TC_DEEP_KS_MAX")) : 8;
+    if (a.ksplit <= 0 && ksplit > ks_cap) ksplit = ks_cap;
     while (ksplit & (ksplit - 1)) ksplit &= ksplit - 1;
     deep = true;
   } else {

@@ -61,6 +61,13 @@ class _DraftBase:
         # by default, the grid form (every SM) on a dedicated draft GPU;
         # SP_DRAFT_FUSED=0 falls back to one graph-replayed step per forward
         self.fused = self.fused_ok and os.environ.get("SP_DRAFT_FUSED", "1") != "0"
+        # set by the Engine when a target stage runs on the draft's GPU: each
+        # request then takes the grid form while no target run is queued (the
+        # GPU is otherwise idle) and the 16-SM cluster form beside one
+        self.shared_gpu = False
+        self._kind = None
+        if self.fused:     # a reused stage may carry another server's choice
+            self.stage.lib.sp_stage_set_draft_kernel(self.stage.h, 0)
         # fused path: rows 0..64 of (argmax, second, conf, max_logit) + err word
         self.rows = torch.zeros((66, 4), dtype=torch.int32, device=draft_model.device)
         self.rows_host = torch.zeros((66, 4), dtype=torch.int32).pin_memory()
@@ -151,6 +158,17 @@ class _DraftBase:
             if err:
                 from . import _lib
                 _lib.raise_device_error(err, "draft")
+
+    def set_exclusive(self, idle: bool) -> None:
+        """Kernel choice for the next request on a shared GPU (see shared_gpu)."""
+        if not (self.fused and self.shared_gpu):
+            return
+        from . import _lib
+        kind = _lib.SP_DRAFT_KIND_GRID if idle else _lib.SP_DRAFT_KIND_CLUSTER
+        if kind != self._kind:
+            _lib.check(self.stage.lib.sp_stage_set_draft_kernel(self.stage.h, kind),
+                       "sp_stage_set_draft_kernel")
+            self._kind = kind
 
     def _mark_start(self) -> None:
         if self.timing:

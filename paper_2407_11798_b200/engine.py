@@ -105,6 +105,22 @@ class ExperimentConfig:
                                          # (engine.py:1027-1030); False asks for
                                          # `microbatch` tokens every time (a GPU
                                          # stage-run costs the same for 1..16 tokens)
+    fold_frontier: Optional[bool] = None  # B200 policy: a frontier token no in-flight
+                                         # run carries waits for the draft and rides
+                                         # in front of its proposals (one run instead
+                                         # of a 1-token run + a speculative run);
+                                         # False = the reference: launch it alone at
+                                         # once (engine.py:1090-1182); None = True on
+                                         # a 1-stage pipeline (nothing to overlap: a
+                                         # run costs a full weight pass for 1..16
+                                         # tokens), False otherwise
+    draft_exclusive: bool = True         # a draft sharing a stage's GPU takes every SM
+                                         # (grid-form kernel) for requests issued while
+                                         # no target run is in flight
+    max_inflight: Optional[int] = None   # B200 policy: no new speculation while this
+                                         # many runs are in flight (0 = unbounded, the
+                                         # reference; partitions still bound it);
+                                         # None = 1 on a 1-stage pipeline, else 0
 
     def validate(self) -> None:
         if self.mode not in MODES:
@@ -127,6 +143,8 @@ class ExperimentConfig:
             raise EngineError("partitions must be >= 2")
         if self.partitions > 32:
             raise EngineError("partitions must be <= 32 (one mask bit each)")
+        if self.max_inflight is not None and self.max_inflight < 0:
+            raise EngineError("max_inflight must be >= 0 (0 = unbounded)")
         if self.gen_len < 1 or self.prompt_len < 1:
             raise EngineError("prompt_len and gen_len must be >= 1")
         if self.prompt_len + self.gen_len > self.max_context:
@@ -367,6 +385,11 @@ class Head:
         self.msgs: Dict[Tuple[int, str], int] = {}
         self.stage_logs: Dict[int, list] = {i + 1: [] for i in range(pipe.n_stages)}
         self.tips: Optional[list] = None   # NS-run tips (truth tables)
+        self.fold = False    # the frontier waits to ride in front of the next proposals
+        self.folded_runs = 0
+        one = pipe.n_stages == 1
+        self.fold_frontier = one if cfg.fold_frontier is None else bool(cfg.fold_frontier)
+        self.max_inflight = (1 if one else 0) if cfg.max_inflight is None else cfg.max_inflight
         from collections import defaultdict
         self.profile: Dict[str, float] = defaultdict(float)   # host seconds by activity
         self._t0 = time.perf_counter()
@@ -383,7 +406,8 @@ class Head:
         self.run_counter += 1
         return self.run_counter
 
-    def _launch(self, batch: Batch, seq_id: int, basis: tuple = ()) -> RunRecord:
+    def _launch(self, batch: Batch, seq_id: int, basis: tuple = (),
+                skippable: bool = True) -> RunRecord:
         rec = RunRecord(run_id=batch.run_id, kind=batch.kind,
                         tokens=tuple(t.token for t in batch.tokens),
                         min_pos=batch.tokens[0].pos, max_pos=batch.tokens[-1].pos,
@@ -392,7 +416,7 @@ class Head:
                                      for slot, i in enumerate(batch.logit_indices)},
                         basis=basis, launch_time=self.now())
         flags = _lib.SP_FWD_CHECK_COVERAGE
-        if batch.kind == SPECULATIVE:
+        if batch.kind == SPECULATIVE and skippable:
             flags |= _lib.SP_FWD_SKIPPABLE
         self.pipe.launch(batch.run_id, KIND_CODE[batch.kind], encode_tokens(batch.tokens),
                          flags, list(batch.logit_indices))
@@ -492,6 +516,9 @@ class Head:
     # -- draft requests -------------------------------------------------------------
     def _draft_request(self, truncate_to: int, feed: Sequence[int], max_tokens: int,
                        cutoff: float) -> None:
+        hint = getattr(self.draft, "set_exclusive", None)
+        if hint is not None and self.cfg.draft_exclusive:
+            hint(self.pipe.in_flight() == 0)     # no target run queued: whole GPU
         self.draft.request(truncate_to, feed, max_tokens, cutoff)
         self._count("DRAFT_REQUEST", 24 + 32 + 8 * len(feed), self.cfg.nodes)
         self.draft_busy = True
@@ -584,7 +611,10 @@ class Head:
     def run_async_speculative(self) -> None:
         self._prefill()
         if not (self.generated >= self.cfg.gen_len or self.terminal):
-            self._launch_ns(self.accepted[-1], with_copy=True)
+            if self.fold_frontier and self.allocator.available() > 0:
+                self.fold = True
+            else:
+                self._launch_ns(self.accepted[-1], with_copy=True)
         prof = self.profile
         clk = time.perf_counter
         while self.generated < self.cfg.gen_len and not self.terminal:
@@ -600,6 +630,12 @@ class Head:
             if not self.draft_busy and self._want_speculation():
                 self._send_draft_request()
                 prof["draft_request"] += clk() - t0
+                continue
+            if self.fold and not self.draft_busy:
+                # nothing will carry the frontier (no partition, cutoff idle,
+                # in-flight cap): launch it alone, as the reference does
+                self.fold = False
+                self._launch_ns(self.accepted[-1], with_copy=True)
                 continue
             self._block_until_message()
             prof["wait"] += clk() - t0
@@ -628,6 +664,9 @@ class Head:
         self._stalled = False
         if self.now() < self.idle_until:
             return False
+        if (self.max_inflight and not self.fold
+                and len(self.fifo) >= self.max_inflight):
+            return False
         return len(self.accepted) + len(self.pending) + 1 <= self.cfg.max_context
 
     @staticmethod
@@ -653,7 +692,7 @@ class Head:
         cp = self._common_prefix(self.mirror, ctx)
         if self.cfg.continuous:
             cap = self.cfg.microbatch
-            if self.cfg.spec_ramp:
+            if self.cfg.spec_ramp and not self.fold:
                 cap = min(cap, max(1, len(self.pending)))
         else:
             cap = self.cfg.tree_cap
@@ -675,9 +714,16 @@ class Head:
             if not self.pipe.ready():
                 self.cutoff.on_speculation_idle()
             self.idle_until = self.now() + self.cfg.idle_poll
+            if self.fold:
+                self.fold = False
+                self._launch_ns(self.accepted[-1], with_copy=True)
             return
         self.cutoff.note_success()
-        self._launch_spec(props)
+        if self.fold:
+            self.fold = False
+            self._launch_folded(props)
+        else:
+            self._launch_spec(props)
         self.spec_since_round += 1
 
     def _carrier_seq(self) -> int:
@@ -702,6 +748,24 @@ class Head:
         self._launch(batch, seq_id=seq, basis=basis)
         self.pending.extend((base + i, t) for i, t in enumerate(props))
         self.pending_tip_seq = seq
+
+    def _launch_folded(self, props: List[int]) -> None:
+        """The frontier token followed by the draft's proposals as ONE run on a
+        fresh partition (sync-speculative's run shape, engine.py:955-970,
+        inside the async pipeline).  The frontier is decided context, so the
+        run is never skipped; its cells reach the canonical sequence and the
+        live partitions through the usual commit (apply_acceptance)."""
+        pos = len(self.accepted) - 1
+        seq = self.allocator.alloc()
+        self._emit_copy(0, (seq,), pos)
+        toks = (BatchToken(self.accepted[-1], pos, frozenset([seq]), True),) + tuple(
+            BatchToken(t, pos + 1 + i, frozenset([seq]), True) for i, t in enumerate(props))
+        batch = Batch(tokens=toks, kind=SPECULATIVE, run_id=self._next_run_id())
+        rec = self._launch(batch, seq_id=seq, skippable=False)
+        rec.judged = 1      # the leading token is accepted context, not a draft
+        self.pending = [(pos + 1 + i, t) for i, t in enumerate(props)]
+        self.pending_tip_seq = seq
+        self.folded_runs += 1
 
     def _handle_completion(self, res) -> None:
         rec = self._pop_record(res)
@@ -736,7 +800,11 @@ class Head:
         self._cancel_stale()
         if self.generated < self.cfg.gen_len and not self.terminal:
             if not self._frontier_carried():
-                self._launch_ns(self.accepted[-1], with_copy=True)
+                if (self.fold_frontier and self.draft is not None
+                        and self.allocator.available() > 0):
+                    self.fold = True    # rides in front of the next proposals
+                else:
+                    self._launch_ns(self.accepted[-1], with_copy=True)
 
     def _frontier_carried(self) -> bool:
         pos = len(self.accepted) - 1
@@ -920,14 +988,21 @@ class Engine:
                                    charge=cfg.draft_charge)
             if prev is not None:
                 srv.forwards = 0
+            srv.shared_gpu = self._shares_gpu()
             self._table_draft = srv
             return srv
         if self.draft is None:
             self.draft = ModelDraftServer(self.draft_model, stream=self._draft_stream,
                                           capacity=min(cfg.capacity, 16 * cfg.max_context))
+            self.draft.shared_gpu = self._shares_gpu()
         else:
             self.draft.reset()
         return self.draft
+
+    def _shares_gpu(self) -> bool:
+        """A target stage of this process runs on the draft's GPU."""
+        dev = self.draft_model.device if self.draft_model is not None else None
+        return any(getattr(st, "device", None) == dev for st in getattr(self.pipe, "stages", []))
 
     def run(self, prompt_seed: Optional[int] = None, prompt: Optional[List[int]] = None,
             mode: Optional[str] = None) -> SimResult:

@@ -182,8 +182,8 @@ def world():
 def test_async_head_randomized_matches_serial(world):
     om, streams = world
     r = np.random.Generator(np.random.PCG64(7))
-    skipped = cancelled = 0
-    for trial in range(40):
+    skipped = cancelled = folded = 0
+    for trial in range(60):
         seed = int(r.integers(0, 3))
         prompt, truth, runner = streams[seed]
         nodes = int(r.integers(2, 5))
@@ -193,13 +193,16 @@ def test_async_head_randomized_matches_serial(world):
             partitions=int(r.integers(2, 9)), microbatch=int(r.integers(1, 5)),
             continuous=bool(r.integers(0, 2)), alpha=float(r.choice([0.0, 0.4, 0.8, 1.0])),
             cutoff=float(r.choice([0.0, 0.3])), cutoff_recovery=float(r.choice([0.0, 0.05])),
-            cutoff_decay=float(r.choice([0.0, 0.05])), spec_ramp=trial % 4 != 3)
+            cutoff_decay=float(r.choice([0.0, 0.05])), spec_ramp=trial % 4 != 3,
+            fold_frontier=[None, True, False][trial % 3],
+            max_inflight=[None, 0, 1, 2, 3][trial % 5])
         pipe = FakePipeline(om, plan_layer_split(4, nodes - 1), cfg.partitions, r)
         draft = FakeDraft(truth, runner, cfg.alpha, trial, 96, r)
         head = Head(cfg, pipe, draft, prompt, 16)
         head.run_async_speculative()
         out = head.accepted[len(prompt):]
         assert out == truth[len(prompt):len(prompt) + cfg.gen_len], (trial, cfg)
+        folded += head.folded_runs
         skipped += pipe.skips
         cancelled += head.cancelled_invalid + head.cancelled_superfluous
         for e in head.cancel_log:
@@ -207,7 +210,7 @@ def test_async_head_randomized_matches_serial(world):
                 assert e.max_pos < e.accepted_len_at_cancel - 1
             else:
                 assert any(p < e.accepted_len_at_cancel and t != truth[p] for p, t in e.chain)
-    assert cancelled > 0 and skipped > 0
+    assert cancelled > 0 and skipped > 0 and folded > 0
 
 
 @pytest.mark.parametrize("mode,nodes", [("iterative", 1), ("pipeline-iterative", 3),
@@ -251,7 +254,8 @@ def test_spec_ramp_caps_requests(world):
     for ramp in (True, False):
         cfg = ExperimentConfig(mode="async-speculative", nodes=2, vocab_size=16, embed_dim=16,
                                target_layers=4, max_context=96, prompt_len=8, gen_len=24,
-                               microbatch=4, alpha=1.0, cutoff=0.0, spec_ramp=ramp)
+                               microbatch=4, alpha=1.0, cutoff=0.0, spec_ramp=ramp,
+                               fold_frontier=False, max_inflight=0)
         r = np.random.Generator(np.random.PCG64(1))
         pipe = FakePipeline(om, [(0, 4)], cfg.partitions, r)
         draft = FakeDraft(truth, runner, cfg.alpha, 0, 96, r)
@@ -270,3 +274,25 @@ def test_spec_ramp_caps_requests(world):
     ramp, flat = [c for c in caps[True] if c > 0], [c for c in caps[False] if c > 0]  # (0: prefill feed)
     assert ramp[0] == 1 and all(1 <= c <= 4 for c in ramp)
     assert set(flat) == {4}
+
+
+def test_fold_frontier_one_stage(world):
+    """B200 policy on a 1-stage pipeline (fold_frontier, max_inflight=1):
+    every run after the prefill carries the frontier token followed by the
+    draft's proposals (sync-speculative's run shape, engine.py:955-970), no
+    run is cancelled, and the stream is the serial one."""
+    om, streams = world
+    prompt, truth, runner = streams[2]
+    r = np.random.Generator(np.random.PCG64(5))
+    cfg = ExperimentConfig(mode="async-speculative", nodes=2, vocab_size=16, embed_dim=16,
+                           target_layers=4, max_context=96, prompt_len=8, gen_len=30,
+                           alpha=0.7, cutoff=0.0)
+    pipe = FakePipeline(om, [(0, 4)], cfg.partitions, r)
+    head = Head(cfg, pipe, FakeDraft(truth, runner, 0.7, 1, 96, r), prompt, 16)
+    assert head.fold_frontier and head.max_inflight == 1     # the 1-stage defaults
+    head.run_async_speculative()
+    assert head.accepted[len(prompt):] == truth[len(prompt):len(prompt) + 30]
+    assert head.folded_runs == head.runs_started - 1 > 0
+    assert head.cancelled_invalid + head.cancelled_superfluous == 0
+    for rec in head.records[1:]:
+        assert len(rec.tokens) >= 2 and rec.tokens[0] == truth[rec.min_pos]

@@ -57,6 +57,7 @@ for M in [int(x) for x in (sys.argv[1:] or ["1", "4", "16"])]:
         a.scratch, a.tickets = scratch.data_ptr(), tick.data_ptr()
         ks = int(os.environ.get("KSPLIT", "0"))
         a.ksplit = ks
+        a.max_ctas = int(os.environ.get("MAXCTAS", "0"))   # a sharing budget (ticket merge)
 
         def tc():
             for w in ws:
@@ -73,6 +74,7 @@ for M in [int(x) for x in (sys.argv[1:] or ["1", "4", "16"])]:
                 _lib.check(lib.sp_gemv(C.byref(g), s))
 
         byt = NL * n * k * 2
-        t1, t2 = timed(tc), timed(cc)
+        t1 = timed(tc)
+        t2 = timed(cc) if not os.environ.get("NOGEMV") else t1
         print(f"M={M:3d} {name:5s} tc {t1*1e3/NL:7.2f} us/launch {byt/t1/1e6:7.0f} GB/s | "
               f"gemv {t2*1e3/NL:7.2f} us {byt/t2/1e6:7.0f} GB/s", flush=True)
