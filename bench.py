@@ -364,12 +364,8 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
                               if os.environ.get("SP_DRAFT_FUSED", "1") != "0" else "per-forward",
                               "spec_ramp": eng.cfg.spec_ramp,
                               "continuous": eng.cfg.continuous,
-                              "fold_frontier": (eng.pipe.n_stages == 1
-                                                if eng.cfg.fold_frontier is None
-                                                else eng.cfg.fold_frontier),
-                              "max_inflight": ((1 if eng.pipe.n_stages == 1 else 0)
-                                               if eng.cfg.max_inflight is None
-                                               else eng.cfg.max_inflight),
+                              "fold_frontier": eng.last_head_policy.get("fold_frontier"),
+                              "max_inflight": eng.last_head_policy.get("max_inflight"),
                               "draft_exclusive": eng.cfg.draft_exclusive,
                               **({"free_draft": True} if not eng.cfg.draft_charge else {})},
                    "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
@@ -456,8 +452,8 @@ def main():
     ap.add_argument("--cutoff", type=float, default=None)
     ap.add_argument("--draft-gpu", default="auto", choices=["auto", "on", "off"],
                     help="N>1: rank 0 = head + dedicated draft GPU, stages on ranks 1..N-1 "
-                         "(the reference's nodes = stages + draft node); auto = on for N>=4 "
-                         "(measured: the shared layout wins at N=2, the dedicated one at N=4)")
+                         "(the reference's nodes = stages + draft node); auto = on "
+                         "(measured: the dedicated layout wins at N=2 and N=4)")
     args = ap.parse_args()
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None and int(os.environ.get("RANK", "0")) == 0:

@@ -467,7 +467,9 @@ def bench_main(args):
     # (n_stages = nodes - 1); otherwise every rank hosts a stage and the draft
     # shares rank 0's GPU
     mode = getattr(args, "draft_gpu", "off")
-    dedicated = world >= 2 and (mode == "on" or (mode == "auto" and world >= 4))
+    # measured (profiles/r02_sweep_n2_n4.txt): the dedicated layout wins at
+    # N=2 (531-540 vs 416 tok/s) and N=4 (590 vs 439)
+    dedicated = world >= 2 and mode in ("on", "auto")
     first = 1 if dedicated else 0
     if dedicated and rank == 0:
         os.environ.setdefault("SP_DRAFT_FUSED", "1")

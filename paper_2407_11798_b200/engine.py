@@ -120,7 +120,9 @@ class ExperimentConfig:
     max_inflight: Optional[int] = None   # B200 policy: no new speculation while this
                                          # many runs are in flight (0 = unbounded, the
                                          # reference; partitions still bound it);
-                                         # None = 1 on a 1-stage pipeline, else 0
+                                         # None = on a 1-stage pipeline 1 (draft on
+                                         # the stage's GPU) or 2 (draft GPU of its
+                                         # own), else 0
 
     def validate(self) -> None:
         if self.mode not in MODES:
@@ -387,9 +389,16 @@ class Head:
         self.tips: Optional[list] = None   # NS-run tips (truth tables)
         self.fold = False    # the frontier waits to ride in front of the next proposals
         self.folded_runs = 0
+        # B200 policy defaults (measured): a 1-stage pipeline
+        # folds the frontier into the next proposals; it keeps one run in
+        # flight when the draft shares the stage's GPU (a concurrent draft
+        # request slows the stage and queues the next fold behind it) and
+        # speculates one run ahead when the draft has a GPU of its own
         one = pipe.n_stages == 1
+        shared = bool(getattr(draft, "shared_gpu", True))
         self.fold_frontier = one if cfg.fold_frontier is None else bool(cfg.fold_frontier)
-        self.max_inflight = (1 if one else 0) if cfg.max_inflight is None else cfg.max_inflight
+        self.max_inflight = (((1 if shared else 2) if one else 0) if cfg.max_inflight is None
+                             else cfg.max_inflight)
         from collections import defaultdict
         self.profile: Dict[str, float] = defaultdict(float)   # host seconds by activity
         self._t0 = time.perf_counter()
@@ -965,6 +974,7 @@ class Engine:
                     if st.device == self.device and st.cfg.arch == "llama":
                         st.set_cta_budget(ctas)
         self._tables: Dict[tuple, tuple] = {}
+        self.last_head_policy: Dict[str, object] = {}
 
     def _make_draft(self, prompt: List[int], prompt_seed: int):
         from .drafting import ModelDraftServer, TableDraftServer
@@ -1020,6 +1030,8 @@ class Engine:
                   "async-speculative": head.run_async_speculative}[cfg.mode]
         runner()
         wall = time.perf_counter() - wall0
+        self.last_head_policy = {"fold_frontier": head.fold_frontier,
+                                 "max_inflight": head.max_inflight}
         metrics = head.build_metrics(wall)
         sent = dict(head.msgs)
         node_logs = dict(head.stage_logs)

@@ -1,0 +1,15 @@
+"""Summarise tools/bench_sweep.sh output: one row per variant."""
+import json
+import sys
+
+for line in open(sys.argv[1]):
+    d = json.loads(line)
+    if "error" in d:
+        print(f"{d['variant']:45s} ERROR {d['error'][-200:]}")
+        continue
+    x = d["line"]
+    print(f"{d['variant']:45s} stages {x['config']['pipeline_stages']} async {x['value']:7.1f} "
+          f"sync {x['sync_speculative_tokens_per_s']:7.1f} iter {x['pipeline_iterative_tokens_per_s']:7.1f} "
+          f"a/s {x['async_over_sync']:.3f} e2e {x['e2e']['value']:7.1f} runs {x['runs_per_step']:6.1f} "
+          f"canc {x['cancelled_runs_per_step']:6.1f} pol {x['config']['engine'].get('fold_frontier')}/"
+          f"{x['config']['engine'].get('max_inflight')}")
