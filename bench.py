@@ -251,6 +251,12 @@ def bench_knobs(args) -> dict:
         kw["draft_charge"] = False
     if getattr(args, "reference_policy", False):   # the reference head, unchanged
         kw.update(fold_frontier=False, max_inflight=0, draft_exclusive=False)
+    if getattr(args, "tree_width", None) is not None:
+        kw["tree_width"] = args.tree_width
+    if getattr(args, "alpha_sibling", None) is not None:
+        kw["alpha_sibling"] = args.alpha_sibling
+    if getattr(args, "depth", None) is not None:     # speculation depth per run
+        kw["microbatch"] = kw["tree_cap"] = args.depth
     if getattr(args, "max_inflight", None) is not None:
         kw["max_inflight"] = args.max_inflight
     if getattr(args, "fold", None) is not None:
@@ -367,6 +373,9 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
                               "fold_frontier": eng.last_head_policy.get("fold_frontier"),
                               "max_inflight": eng.last_head_policy.get("max_inflight"),
                               "draft_exclusive": eng.cfg.draft_exclusive,
+                              "tree_width": eng.cfg.tree_width,
+                              **({"alpha_sibling": eng.cfg.alpha_sibling}
+                                 if eng.cfg.tree_width > 1 else {}),
                               **({"free_draft": True} if not eng.cfg.draft_charge else {})},
                    "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
         "itl_ms": round(itl * 1e3, 3),
@@ -446,6 +455,14 @@ def main():
                     help="the reference head's scheduling (no frontier folding, unbounded "
                          "in-flight speculation, draft always on the 16-SM cluster kernel)")
     ap.add_argument("--max-inflight", type=int, default=None)
+    ap.add_argument("--tree-width", type=int, default=None, choices=[1, 2],
+                    help="1 = chain speculation; 2 = + the draft's runner-up as a sibling "
+                         "leaf per proposal (configs[4] sweep)")
+    ap.add_argument("--alpha-sibling", type=float, default=None,
+                    help="synthetic draft: P(runner-up is the target's token | first choice "
+                         "is not), tree width 2")
+    ap.add_argument("--depth", type=int, default=None, choices=[1, 2, 3, 4],
+                    help="speculation depth (microbatch = tree_cap)")
     ap.add_argument("--fold", choices=["on", "off"], default=None)
     ap.add_argument("--microbatch", type=int, default=None)
     ap.add_argument("--partitions", type=int, default=None)

@@ -73,6 +73,7 @@ class _DraftBase:
         self.rows_host = torch.zeros((66, 4), dtype=torch.int32).pin_memory()
         self.event = torch.cuda.Event()
         self.tokens: List[int] = []
+        self.seconds: tuple = ()   # the draft's runner-up per proposal (tree speculation)
         self._pending = None
         self.forwards = 0          # draft-model forwards issued (cost accounting)
         # diagnostics (SP_RUN_TIMING=1): timing events around each request
@@ -232,13 +233,14 @@ class ModelDraftServer(_DraftBase):
             self._check_fused_err()
         else:
             self._check_err()
+        self.seconds = ()
         if budget == 0:
             return (), ()
         if fused:
             r = self.rows_host[:budget + 1].numpy().view(RES_DTYPE).reshape(-1)
         else:
             r = self.res_host[:budget + 1, 1].numpy().view(RES_DTYPE).reshape(-1)
-        toks, confs = [], []
+        toks, confs, secs = [], [], []
         for j in range(budget):
             conf = np.float32(r[j]["c"])
             if j == 0 and (conf < 0 or r[0]["a"] < 0):
@@ -247,7 +249,9 @@ class ModelDraftServer(_DraftBase):
                 break
             toks.append(int(r[j]["a"]))
             confs.append(float(conf))
+            secs.append(int(r[j]["b"]))
         self.tokens.extend(toks)
+        self.seconds = tuple(secs)
         return tuple(toks), tuple(confs)
 
 
@@ -262,12 +266,18 @@ class TableDraftServer(_DraftBase):
 
     def __init__(self, draft_model, truth: Sequence[int], runner: Sequence[int],
                  alpha: float, seed: int, stream=None, capacity=None,
-                 charge: bool = True, max_tokens: int = 256, stage=None):
+                 charge: bool = True, max_tokens: int = 256, stage=None,
+                 alpha_sibling: float = 0.0):
         super().__init__(draft_model, stream, capacity, max_tokens, stage)
         if not 0.0 <= alpha <= 1.0:
             raise SpeculationError(f"alpha must be in [0,1], got {alpha}")
         self.alpha = float(alpha)
         self.rng = np.random.Generator(np.random.PCG64(seed))
+        # tree speculation: the runner-up choice per proposal.  A separate
+        # stream, so chain emissions stay the reference's draw sequence
+        self.alpha_sibling = float(alpha_sibling)
+        self.rng2 = np.random.Generator(np.random.PCG64(seed + 0x5EED))
+        self.vocab = draft_model.config.vocab_size
         self.truth = list(truth)
         self.runner = list(runner)
         self.charge = charge
@@ -304,17 +314,34 @@ class TableDraftServer(_DraftBase):
         props = []
         if budget > 0 and len(self.tokens) == 0:
             raise SpeculationError("draft has no context yet")
+        secs = []
         if budget > 0 and not self.alpha < cutoff:
             for _ in range(budget):
                 p = len(self.tokens)
                 best = self.truth[p] if p < len(self.truth) else 0
                 second = self.runner[p] if p < len(self.runner) else 1
                 tok = best if self.rng.random() < self.alpha else second
+                if self.alpha_sibling > 0.0:
+                    # the runner-up: the other of (greedy, runner-up) when the
+                    # first choice is the greedy token; when it is not, the
+                    # greedy token with probability alpha_sibling, else a
+                    # third token (off the greedy path either way)
+                    hit = self.rng2.random() < self.alpha_sibling
+                    if tok == best:
+                        alt = second
+                    elif hit:
+                        alt = best
+                    else:
+                        alt = (best + 1) % self.vocab
+                        if alt == tok:
+                            alt = (best + 2) % self.vocab
+                    secs.append(alt)
                 if self.charge and not self.fused:
                     self._forward([tok], p)
                 self.tokens.append(tok)
                 self._retrack(p)
                 props.append(tok)
+        self.seconds = tuple(secs)
         if self.charge and self.fused and (feed or props):
             # the forwards a real draft would run, as one persistent launch
             self._launch_chain(feed, feed_pos, len(props), 0.0, step_tokens=props)

@@ -32,7 +32,8 @@ from .model import (KIND_CODE, NON_SPECULATIVE, PREFILL, SPECULATIVE, Batch,
                     BatchToken, ModelConfig, encode_tokens, greedy_sample,
                     llama_config, sample_prompt)
 from .speculation import CutoffController
-from .verify import INVALID, apply_acceptance, detect_stale_runs, verify_run
+from .verify import (INVALID, VerifyResult, apply_acceptance, detect_stale_runs,
+                     verify_run)
 
 MODES = ("iterative", "pipeline-iterative", "sync-speculative", "async-speculative")
 
@@ -114,6 +115,15 @@ class ExperimentConfig:
                                          # a 1-stage pipeline (nothing to overlap: a
                                          # run costs a full weight pass for 1..16
                                          # tokens), False otherwise
+    tree_width: int = 1                  # 1 = chain speculation (the reference); 2 =
+                                         # every proposal also carries the draft's
+                                         # runner-up as a sibling leaf (same position,
+                                         # own partition), verified greedily in the
+                                         # same run (a B200 run costs the same for
+                                         # 1..16 tokens)
+    alpha_sibling: float = 0.4           # synthetic draft, tree_width 2: probability
+                                         # its runner-up is the target's greedy token
+                                         # when its first choice is not
     draft_exclusive: bool = True         # a draft sharing a stage's GPU takes every SM
                                          # (grid-form kernel) for requests issued while
                                          # no target run is in flight
@@ -145,6 +155,10 @@ class ExperimentConfig:
             raise EngineError("partitions must be >= 2")
         if self.partitions > 32:
             raise EngineError("partitions must be <= 32 (one mask bit each)")
+        if self.tree_width not in (1, 2):
+            raise EngineError("tree_width must be 1 (chain) or 2 (chain + runner-up siblings)")
+        if not 0.0 <= self.alpha_sibling <= 1.0:
+            raise EngineError("alpha_sibling must be in [0, 1]")
         if self.max_inflight is not None and self.max_inflight < 0:
             raise EngineError("max_inflight must be >= 0 (0 = unbounded)")
         if self.gen_len < 1 or self.prompt_len < 1:
@@ -250,6 +264,13 @@ class RunRecord:
     status: str = IN_FLIGHT
     launch_time: float = 0.0
     judged: int = 0
+    # tree runs: pos -> (token, partition, logits slot) of the sibling leaf
+    # at that position, and every partition the run wrote under
+    siblings: Dict[int, Tuple[int, int, int]] = field(default_factory=dict)
+    tree_seqs: tuple = ()
+
+    def partitions(self) -> tuple:
+        return tuple(q for q in ((self.seq_id,) + self.tree_seqs) if q != 0)
 
     def chain(self):
         for pos, tok in self.basis:
@@ -389,6 +410,8 @@ class Head:
         self.tips: Optional[list] = None   # NS-run tips (truth tables)
         self.fold = False    # the frontier waits to ride in front of the next proposals
         self.folded_runs = 0
+        self.tree_siblings = self.sibling_hits = 0
+        self.last_seconds: tuple = ()
         # B200 policy defaults (measured): a 1-stage pipeline
         # folds the frontier into the next proposals; it keeps one run in
         # flight when the draft shares the stage's GPU (a concurrent draft
@@ -416,14 +439,24 @@ class Head:
         return self.run_counter
 
     def _launch(self, batch: Batch, seq_id: int, basis: tuple = (),
-                skippable: bool = True) -> RunRecord:
+                skippable: bool = True, n_chain: Optional[int] = None,
+                tree_seqs: tuple = ()) -> RunRecord:
+        """``n_chain``: the first n_chain tokens are the run's chain; the rest
+        are sibling leaves (tree runs), each at the position of the chain
+        token it is an alternative to."""
+        nc = len(batch.tokens) if n_chain is None else n_chain
+        chain = batch.tokens[:nc]
+        slots = {i: slot for slot, i in enumerate(batch.logit_indices)}
         rec = RunRecord(run_id=batch.run_id, kind=batch.kind,
-                        tokens=tuple(t.token for t in batch.tokens),
-                        min_pos=batch.tokens[0].pos, max_pos=batch.tokens[-1].pos,
+                        tokens=tuple(t.token for t in chain),
+                        min_pos=chain[0].pos, max_pos=chain[-1].pos,
                         seq_id=seq_id,
-                        logit_slots={batch.tokens[i].pos: slot
-                                     for slot, i in enumerate(batch.logit_indices)},
-                        basis=basis, launch_time=self.now())
+                        logit_slots={chain[i].pos: slots[i] for i in range(nc) if i in slots},
+                        basis=basis, launch_time=self.now(),
+                        siblings={batch.tokens[i].pos: (batch.tokens[i].token,
+                                                        min(batch.tokens[i].seqs), slots[i])
+                                  for i in range(nc, len(batch.tokens))},
+                        tree_seqs=tuple(tree_seqs))
         flags = _lib.SP_FWD_CHECK_COVERAGE
         if batch.kind == SPECULATIVE and skippable:
             flags |= _lib.SP_FWD_SKIPPABLE
@@ -534,6 +567,7 @@ class Head:
 
     def _draft_reply(self):
         toks, confs = self.draft.reply()
+        self.last_seconds = tuple(getattr(self.draft, "seconds", ()) or ())
         self.draft_busy = False
         self._count("DRAFT_REPLY", 24 + 8 + 16 * len(toks), 0)
         return toks, confs
@@ -595,6 +629,31 @@ class Head:
         while self.generated < self.cfg.gen_len and not self.terminal:
             drafts, _ = self._draft_round_trip(self.cfg.tree_cap, self.cutoff.base)
             pos = len(self.accepted) - 1
+            if self.cfg.tree_width >= 2 and self.allocator.available() > 0:
+                # tree round: frontier + chain + sibling leaves on partitions,
+                # committed like an async run
+                seq = self.allocator.alloc()
+                toks, n_chain, tseqs = self._tree_tokens(
+                    (tok,), pos + 1, list(drafts), self.last_seconds[:len(drafts)], seq)
+                self._emit_copy(0, (seq,) + tseqs, pos)
+                batch = Batch(tokens=toks, kind=SPECULATIVE, run_id=self._next_run_id())
+                rec = self._launch(batch, seq_id=seq, skippable=False, n_chain=n_chain,
+                                   tree_seqs=tseqs)
+                rec.judged = 1
+                res = self._recv()
+                got = self._pop_record(res)
+                got.status = COMPLETED
+                result, src = self._verify(got, res.rows)
+                self._judge_walked(got, result)
+                for t in result.accepted:
+                    self._accept(t)
+                if result.next_token is not None:
+                    self._accept(result.next_token)
+                self._commit(got, result, src)
+                if self.terminal:
+                    break
+                tok = self.accepted[-1]
+                continue
             toks = [BatchToken(tok, pos, frozenset([0]), True)]
             toks += [BatchToken(d, pos + 1 + i, frozenset([0]), True)
                      for i, d in enumerate(drafts)]
@@ -728,11 +787,12 @@ class Head:
                 self._launch_ns(self.accepted[-1], with_copy=True)
             return
         self.cutoff.note_success()
+        seconds = self.last_seconds[:len(props)]
         if self.fold:
             self.fold = False
-            self._launch_folded(props)
+            self._launch_folded(props, seconds)
         else:
-            self._launch_spec(props)
+            self._launch_spec(props, seconds)
         self.spec_since_round += 1
 
     def _carrier_seq(self) -> int:
@@ -745,20 +805,47 @@ class Head:
                 return rec.seq_id
         return 0
 
-    def _launch_spec(self, props: List[int]) -> None:
+    def _tree_tokens(self, lead: tuple, base: int, props: List[int], seconds, seq: int):
+        """Batch tokens of a (tree) run: ``lead`` (decided frontier token at
+        base - 1, or nothing) + the proposals at base.. on partition ``seq``,
+        then -- tree_width 2 -- the draft's runner-up for proposal i as a
+        sibling leaf at base + i on a partition of its own.  Visibility
+        follows the reference's rule (build_tree_mask, model.py:262-284: a
+        cell is seen iff it is earlier and shares a sequence): chain tokens
+        before depth i also carry the sibling's partition, so the sibling
+        sees exactly the context its chain twin sees."""
+        sibs = []
+        if self.cfg.tree_width >= 2 and seconds:
+            for i, (d, t2) in enumerate(zip(props, seconds)):
+                if t2 is None or t2 < 0 or t2 == d or self.allocator.available() == 0:
+                    continue
+                sibs.append((i, int(t2), self.allocator.alloc()))
+        tseqs = tuple(q for _, _, q in sibs)
+        toks = []
+        if lead:
+            toks.append(BatchToken(lead[0], base - 1, frozenset((seq,) + tseqs), True))
+        for m, t in enumerate(props):
+            extra = tuple(q for i, _, q in sibs if i > m)
+            toks.append(BatchToken(t, base + m, frozenset((seq,) + extra), True))
+        n_chain = len(toks)
+        for i, t2, q in sibs:
+            toks.append(BatchToken(t2, base + i, frozenset([q]), True))
+            self.tree_siblings += 1
+        return tuple(toks), n_chain, tseqs
+
+    def _launch_spec(self, props: List[int], seconds=()) -> None:
         base = len(self.accepted) + len(self.pending)
         seq = self.allocator.alloc()
         src = self.pending_tip_seq if self.pending else self._carrier_seq()
-        self._emit_copy(src, (seq,), base)
+        toks, n_chain, tseqs = self._tree_tokens((), base, props, seconds, seq)
+        self._emit_copy(src, (seq,) + tseqs, base)
         basis = tuple(self.pending)
-        toks = tuple(BatchToken(t, base + i, frozenset([seq]), True)
-                     for i, t in enumerate(props))
         batch = Batch(tokens=toks, kind=SPECULATIVE, run_id=self._next_run_id())
-        self._launch(batch, seq_id=seq, basis=basis)
+        self._launch(batch, seq_id=seq, basis=basis, n_chain=n_chain, tree_seqs=tseqs)
         self.pending.extend((base + i, t) for i, t in enumerate(props))
         self.pending_tip_seq = seq
 
-    def _launch_folded(self, props: List[int]) -> None:
+    def _launch_folded(self, props: List[int], seconds=()) -> None:
         """The frontier token followed by the draft's proposals as ONE run on a
         fresh partition (sync-speculative's run shape, engine.py:955-970,
         inside the async pipeline).  The frontier is decided context, so the
@@ -766,41 +853,80 @@ class Head:
         live partitions through the usual commit (apply_acceptance)."""
         pos = len(self.accepted) - 1
         seq = self.allocator.alloc()
-        self._emit_copy(0, (seq,), pos)
-        toks = (BatchToken(self.accepted[-1], pos, frozenset([seq]), True),) + tuple(
-            BatchToken(t, pos + 1 + i, frozenset([seq]), True) for i, t in enumerate(props))
+        toks, n_chain, tseqs = self._tree_tokens((self.accepted[-1],), pos + 1, props,
+                                                 seconds, seq)
+        self._emit_copy(0, (seq,) + tseqs, pos)
         batch = Batch(tokens=toks, kind=SPECULATIVE, run_id=self._next_run_id())
-        rec = self._launch(batch, seq_id=seq, skippable=False)
+        rec = self._launch(batch, seq_id=seq, skippable=False, n_chain=n_chain,
+                           tree_seqs=tseqs)
         rec.judged = 1      # the leading token is accepted context, not a draft
         self.pending = [(pos + 1 + i, t) for i, t in enumerate(props)]
         self.pending_tip_seq = seq
         self.folded_runs += 1
 
+    def _verify(self, rec: RunRecord, rows):
+        """verify_run (verify.py:43-124) plus, for tree runs, the sibling
+        step: where the chain's first mismatch is, a sibling leaf equal to
+        the target's greedy token is accepted and its own row donates the
+        next token.  Returns (result, partition holding the accepted path)."""
+        result = verify_run(rec, rows, self.accepted, eos_token=self.cfg.eos_token)
+        if not (result.mismatch and rec.siblings):
+            return result, rec.seq_id
+        p = result.matched_end
+        sib = rec.siblings.get(p)
+        if sib is None or sib[0] != result.next_token:
+            return result, rec.seq_id
+        tok, q, slot = sib
+        self.sibling_hits += 1
+        acc = result.accepted + (tok,)
+        eos = self.cfg.eos_token
+        if eos is not None and tok == eos:
+            return VerifyResult(acc, len(acc), None, True, result.examined, False, p + 1), q
+        nxt = greedy_sample(rows[slot])
+        return VerifyResult(acc, len(acc), nxt, eos is not None and nxt == eos,
+                            result.examined, False, p + 1), q
+
+    def _commit(self, rec: RunRecord, result, src: int) -> None:
+        """apply_acceptance (verify.py:156-178) for chain and tree runs: the
+        accepted cells (chain prefix, or prefix + sibling from the sibling's
+        partition) reach the canonical sequence and every other live
+        partition; every partition of the run is released."""
+        cmds: List[Tuple[str, tuple]] = []
+        if not rec.tree_seqs:
+            apply_acceptance(result, rec, lambda op, args: cmds.append((op, args)),
+                             self.allocator.live())
+        elif result.matched_end > rec.min_pos:
+            mine = set(rec.partitions())
+            dsts = tuple(sorted({0, *self.allocator.live()} - mine))
+            cmds.append(("copy", (src, dsts, result.matched_end)))
+        for op, args in cmds:
+            if op == "copy":
+                self._emit_copy(*args)
+            else:
+                self._emit_remove(*args)
+        for q in rec.tree_seqs:
+            self._emit_remove(q, 0)
+        if rec.tree_seqs and rec.seq_id != 0:
+            self._emit_remove(rec.seq_id, 0)
+        for q in rec.partitions():
+            self.allocator.free(q)
+
     def _handle_completion(self, res) -> None:
         rec = self._pop_record(res)
         if rec.status in (CANCELLED_INVALID, CANCELLED_SUPERFLUOUS, DRAINED):
-            if rec.seq_id != 0:
-                self._emit_remove(rec.seq_id, 0)
-                self.allocator.free(rec.seq_id)
+            for q in rec.partitions():
+                self._emit_remove(q, 0)
+                self.allocator.free(q)
             return
         rec.status = COMPLETED
-        result = verify_run(rec, res.rows, self.accepted, eos_token=self.cfg.eos_token)
+        result, src = self._verify(rec, res.rows)
         self._judge_walked(rec, result)
         new_tokens = list(result.accepted)
         if result.next_token is not None:
             new_tokens.append(result.next_token)
         for t in new_tokens:
             self._accept(t)
-        cmds: List[Tuple[str, tuple]] = []
-        apply_acceptance(result, rec, lambda op, args: cmds.append((op, args)),
-                         self.allocator.live())
-        for op, args in cmds:
-            if op == "copy":
-                self._emit_copy(*args)
-            else:
-                self._emit_remove(*args)
-        if rec.seq_id != 0:
-            self.allocator.free(rec.seq_id)
+        self._commit(rec, result, src)
         if not new_tokens:
             return
         self._rebase_pending()
@@ -865,8 +991,9 @@ class Head:
         while self.fifo:
             res = self._recv()
             rec = self._pop_record(res)
-            if rec.seq_id != 0 and rec.seq_id in self.allocator.live():
-                self.allocator.free(rec.seq_id)
+            for q in rec.partitions():
+                if q in self.allocator.live():
+                    self.allocator.free(q)
         if self.draft_busy:
             self._draft_reply()
 
@@ -995,7 +1122,9 @@ class Engine:
                                    stream=self._draft_stream,
                                    capacity=min(cfg.capacity, 16 * cfg.max_context),
                                    stage=None if prev is None else prev.stage,
-                                   charge=cfg.draft_charge)
+                                   charge=cfg.draft_charge,
+                                   alpha_sibling=(cfg.alpha_sibling if cfg.tree_width >= 2
+                                                  else 0.0))
             if prev is not None:
                 srv.forwards = 0
             srv.shared_gpu = self._shares_gpu()

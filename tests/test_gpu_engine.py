@@ -268,3 +268,28 @@ def test_persistent_stage_kernel_streams(sp):
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("mode,nodes", [("sync-speculative", 4), ("async-speculative", 4),
+                                        ("async-speculative", 2)])
+@pytest.mark.parametrize("seed", [5, 21])
+def test_tree_speculation_streams(sp, golden, mode, nodes, seed):
+    """Tree speculation (tree_width 2: chain + the draft's runner-up as a
+    sibling leaf per proposal, tree-masked through partition membership)
+    emits the reference's serial greedy stream on the fp32 toy decoder."""
+    res = sp.simulate(cfg(sp, mode=mode, nodes=nodes, prompt_seed=seed, tree_width=2,
+                          draft_backend="synthetic", alpha=0.5, alpha_sibling=0.6,
+                          partitions=16))
+    assert res.tokens == _golden_stream(golden, seed)
+
+
+def test_tree_speculation_llama_deep(sp):
+    """Same on the bf16 llama path (tcgen05 GEMMs, tree-masked attention):
+    equals the iterative stream of the same weights, and siblings land."""
+    it = sp.simulate(deep(sp, mode="iterative", nodes=1, gen_len=48)).tokens
+    for mode, nodes in (("sync-speculative", 3), ("async-speculative", 3),
+                        ("async-speculative", 2)):
+        res = sp.simulate(deep(sp, mode=mode, nodes=nodes, draft_backend="synthetic",
+                               alpha=0.5, tree_width=2, alpha_sibling=0.6, partitions=16,
+                               gen_len=48))
+        assert res.tokens == it, mode

@@ -119,9 +119,12 @@ class FakePipeline:
 class FakeDraft:
     """SyntheticDraft semantics over the oracle's greedy table, random latency."""
 
-    def __init__(self, truth, runner, alpha, seed, max_context, rng):
+    def __init__(self, truth, runner, alpha, seed, max_context, rng, alpha_sibling=0.0):
         self.truth, self.runner, self.alpha = truth, runner, alpha
         self.g = np.random.Generator(np.random.PCG64(seed))
+        self.g2 = np.random.Generator(np.random.PCG64(seed + 99))
+        self.alpha_sibling = alpha_sibling
+        self.seconds = ()
         self.max_context, self.rng = max_context, rng
         self.tokens, self.pending = [], None
         self.forwards = 0
@@ -136,7 +139,7 @@ class FakeDraft:
         if max_tokens and not self.tokens:
             raise errors.SpeculationError("draft has no context yet")
         budget = max(0, min(max_tokens, self.max_context - len(self.tokens), 4))
-        props = []
+        props, secs = [], []
         if budget and self.alpha >= cutoff:
             for _ in range(budget):
                 p = len(self.tokens)
@@ -146,9 +149,13 @@ class FakeDraft:
                 tok = best if self.g.random() < self.alpha else second
                 if not on:
                     tok = second
+                hit = self.g2.random() < self.alpha_sibling
+                secs.append(second if tok == best else best if hit else (best + 1) % 16
+                            if (best + 1) % 16 != tok else (best + 2) % 16)
                 self.tokens.append(tok)
                 props.append(tok)
         self.pending = tuple(props)
+        self.seconds = tuple(secs)
 
     def ready(self):
         return self.pending is not None and self.rng.random() < 0.5
@@ -182,7 +189,7 @@ def world():
 def test_async_head_randomized_matches_serial(world):
     om, streams = world
     r = np.random.Generator(np.random.PCG64(7))
-    skipped = cancelled = folded = 0
+    skipped = cancelled = folded = sib_hits = 0
     for trial in range(60):
         seed = int(r.integers(0, 3))
         prompt, truth, runner = streams[seed]
@@ -195,14 +202,16 @@ def test_async_head_randomized_matches_serial(world):
             cutoff=float(r.choice([0.0, 0.3])), cutoff_recovery=float(r.choice([0.0, 0.05])),
             cutoff_decay=float(r.choice([0.0, 0.05])), spec_ramp=trial % 4 != 3,
             fold_frontier=[None, True, False][trial % 3],
-            max_inflight=[None, 0, 1, 2, 3][trial % 5])
+            max_inflight=[None, 0, 1, 2, 3][trial % 5], tree_width=1 + (trial % 2))
         pipe = FakePipeline(om, plan_layer_split(4, nodes - 1), cfg.partitions, r)
-        draft = FakeDraft(truth, runner, cfg.alpha, trial, 96, r)
+        draft = FakeDraft(truth, runner, cfg.alpha, trial, 96, r,
+                          alpha_sibling=0.5 if cfg.tree_width == 2 else 0.0)
         head = Head(cfg, pipe, draft, prompt, 16)
         head.run_async_speculative()
         out = head.accepted[len(prompt):]
         assert out == truth[len(prompt):len(prompt) + cfg.gen_len], (trial, cfg)
         folded += head.folded_runs
+        sib_hits += head.sibling_hits
         skipped += pipe.skips
         cancelled += head.cancelled_invalid + head.cancelled_superfluous
         for e in head.cancel_log:
@@ -210,7 +219,7 @@ def test_async_head_randomized_matches_serial(world):
                 assert e.max_pos < e.accepted_len_at_cancel - 1
             else:
                 assert any(p < e.accepted_len_at_cancel and t != truth[p] for p, t in e.chain)
-    assert cancelled > 0 and skipped > 0 and folded > 0
+    assert cancelled > 0 and skipped > 0 and folded > 0 and sib_hits > 0
 
 
 @pytest.mark.parametrize("mode,nodes", [("iterative", 1), ("pipeline-iterative", 3),
@@ -296,3 +305,37 @@ def test_fold_frontier_one_stage(world):
     assert head.cancelled_invalid + head.cancelled_superfluous == 0
     for rec in head.records[1:]:
         assert len(rec.tokens) >= 2 and rec.tokens[0] == truth[rec.min_pos]
+
+
+@pytest.mark.parametrize("mode,nodes", [("sync-speculative", 3), ("async-speculative", 2),
+                                        ("async-speculative", 4)])
+def test_tree_speculation_matches_serial(world, mode, nodes):
+    """tree_width 2: every proposal carries the draft's runner-up as a
+    sibling leaf on its own partition (visibility per build_tree_mask,
+    model.py:262-284); the head accepts a sibling that equals the target's
+    greedy token and takes its row's prediction as the next token.  Streams
+    equal the serial ones, siblings get accepted, and a tree round accepts
+    more tokens per run than a chain round."""
+    om, streams = world
+    prompt, truth, runner = streams[0]
+    per_run = {}
+    for width in (1, 2):
+        r = np.random.Generator(np.random.PCG64(11))
+        cfg = ExperimentConfig(mode=mode, nodes=nodes, vocab_size=16, embed_dim=16,
+                               target_layers=4, max_context=96, prompt_len=8, gen_len=36,
+                               alpha=0.5, cutoff=0.0, tree_width=width, partitions=16)
+        pipe = FakePipeline(om, plan_layer_split(4, cfg.n_stages()), cfg.partitions, r)
+        draft = FakeDraft(truth, runner, 0.5, 4, 96, r, alpha_sibling=0.6 if width == 2 else 0.0)
+        head = Head(cfg, pipe, draft, prompt, 16)
+        {"sync-speculative": head.run_sync_speculative,
+         "async-speculative": head.run_async_speculative}[mode]()
+        assert head.accepted[len(prompt):] == truth[len(prompt):len(prompt) + 36], width
+        completed = sum(1 for rec in head.records if rec.status == "completed")
+        per_run[width] = 36 / completed
+        if width == 2:
+            assert head.tree_siblings > 0
+            # (a 3-stage pipeline completes few speculative runs on 36 tokens)
+            assert head.sibling_hits > 0 or nodes > 2
+            assert not head.allocator.live()          # every partition released
+    if mode == "sync-speculative":
+        assert per_run[2] > per_run[1]

@@ -12,4 +12,5 @@ for line in open(sys.argv[1]):
           f"sync {x['sync_speculative_tokens_per_s']:7.1f} iter {x['pipeline_iterative_tokens_per_s']:7.1f} "
           f"a/s {x['async_over_sync']:.3f} e2e {x['e2e']['value']:7.1f} runs {x['runs_per_step']:6.1f} "
           f"canc {x['cancelled_runs_per_step']:6.1f} pol {x['config']['engine'].get('fold_frontier')}/"
-          f"{x['config']['engine'].get('max_inflight')}")
+          f"{x['config']['engine'].get('max_inflight')} w{x['config']['engine'].get('tree_width')}"
+          f" d{x['config']['engine'].get('microbatch')}")
