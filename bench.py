@@ -32,6 +32,12 @@ sys.path.insert(0, ROOT)
 
 TARGET, DRAFT = "llama2-7b", "llama-160m"
 ALPHA = 0.66          # paper's observed acceptance for a 7B pair
+# BASELINE.json configs by (target, draft) shape
+WORKLOADS = {("llama2-7b", "llama-160m"): "configs[1]: Llama-2-7B-shape target + 160M-shape draft",
+             ("llama2-13b", "tinyllama-1.1b"): "configs[2]: Llama-2-13B-shape target + "
+                                               "TinyLlama-1.1B-shape draft",
+             ("llama2-70b", "tinyllama-1.1b"): "configs[3]: Llama-2-70B-shape target + "
+                                               "1.1B-shape draft"}
 PROMPT_LEN, GEN_LEN, MAX_CTX = 128, 512, 1024
 
 
@@ -100,19 +106,20 @@ class Clocks:
 # CPU baseline: the reference algorithm (float64 oracle) on host cores
 # ---------------------------------------------------------------------------
 
-def cpu_baseline(n_decode: int = 3, layers: int = 2, prompt_len: int = 16) -> dict:
+def cpu_baseline(n_decode: int = 3, layers: int = 2, prompt_len: int = 16,
+                 shape: str = TARGET) -> dict:
     """The oracle's fp64 forward timed with every host thread BLAS can use
     (torchrun exports OMP_NUM_THREADS=1; the reference arm must not inherit it)."""
     import numpy  # noqa: F401  (load BLAS first: threadpoolctl only sees loaded libraries)
     try:
         from threadpoolctl import threadpool_limits
         with threadpool_limits(limits=os.cpu_count() or 1):
-            return _cpu_baseline(n_decode, layers, prompt_len)
+            return _cpu_baseline(n_decode, layers, prompt_len, shape)
     except ImportError:
-        return _cpu_baseline(n_decode, layers, prompt_len)
+        return _cpu_baseline(n_decode, layers, prompt_len, shape)
 
 
-def _cpu_baseline(n_decode: int, layers: int, prompt_len: int) -> dict:
+def _cpu_baseline(n_decode: int, layers: int, prompt_len: int, shape: str = TARGET) -> dict:
     import numpy as np
     from oracle import model as OM
     from oracle.kvcache import OracleCache
@@ -121,16 +128,23 @@ def _cpu_baseline(n_decode: int, layers: int, prompt_len: int) -> dict:
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count() or 1
-    d, f, V, H = 4096, 11008, 32000, 32
+    from paper_2407_11798_b200.model import LLAMA_SHAPES
+    sh = LLAMA_SHAPES[shape]
+    d, f, V, H = sh["embed_dim"], sh["ffn_dim"], sh["vocab_size"], sh["n_heads"]
+    KH, NL = sh["n_kv_heads"], sh["n_layers"]
+    kvd = d // H * KH
+    if d >= 8192:          # 70B width: one fp64 layer is ~6 GB of host memory
+        layers = 1
     r = np.random.Generator(np.random.PCG64(0))
     cfg = OM.OracleConfig(vocab_size=V, embed_dim=d, n_layers=layers, n_heads=H,
-                          max_context=1024, arch="llama", ffn_dim=f)
+                          max_context=1024, arch="llama", ffn_dim=f, n_kv_heads=KH)
     lw = []
+    sd, sf = d ** -0.5, f ** -0.5
     for _ in range(layers):
-        lw.append(dict(wq=r.standard_normal((d, d)) / 64, wk=r.standard_normal((d, d)) / 64,
-                       wv=r.standard_normal((d, d)) / 64, wo=r.standard_normal((d, d)) / 64,
-                       wg=r.standard_normal((d, f)) / 64, wu=r.standard_normal((d, f)) / 64,
-                       wd=r.standard_normal((f, d)) / 105, attn_norm=np.ones(d),
+        lw.append(dict(wq=r.standard_normal((d, d)) * sd, wk=r.standard_normal((d, kvd)) * sd,
+                       wv=r.standard_normal((d, kvd)) * sd, wo=r.standard_normal((d, d)) * sd,
+                       wg=r.standard_normal((d, f)) * sd, wu=r.standard_normal((d, f)) * sd,
+                       wd=r.standard_normal((f, d)) * sf, attn_norm=np.ones(d),
                        mlp_norm=np.ones(d)))
     emb = r.standard_normal((V, d))
     w_out = r.standard_normal((d, V)) / 64
@@ -149,12 +163,12 @@ def _cpu_baseline(n_decode: int, layers: int, prompt_len: int) -> dict:
     OM.logits(m, x, tok)
     t_head = time.perf_counter() - t0
     per_layer = statistics.median(t_layers) / layers
-    per_token = per_layer * 32 + t_head
+    per_token = per_layer * NL + t_head
     return {"value": 1.0 / per_token, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": (f"oracle fp64 llama forward, {layers} layers at 7B width "
-                       f"(d=4096, ffn=11008), {n_decode} decode tokens after a "
-                       f"{prompt_len}-token prompt, + LM head V=32000; per-token time "
-                       f"extrapolated to 32 layers ({per_layer*1e3:.1f} ms/layer, "
+            "sample": (f"oracle fp64 llama forward, {layers} layers at {shape} width "
+                       f"(d={d}, ffn={f}, kv heads {KH}/{H}), {n_decode} decode tokens after a "
+                       f"{prompt_len}-token prompt, + LM head V={V}; per-token time "
+                       f"extrapolated to {NL} layers ({per_layer*1e3:.1f} ms/layer, "
                        f"head {t_head*1e3:.1f} ms)"),
             "ms_per_token": per_token * 1e3}
 
@@ -272,8 +286,8 @@ def run_ours(args) -> dict:
         from paper_2407_11798_b200 import dist
         return dist.bench_main(args)
     torch.cuda.set_device(0)
-    cfg = ExperimentConfig(mode="async-speculative", nodes=2, target_shape=TARGET,
-                           draft_shape=DRAFT, draft_backend="synthetic", alpha=ALPHA,
+    cfg = ExperimentConfig(mode="async-speculative", nodes=2, target_shape=args.target,
+                           draft_shape=args.draft, draft_backend="synthetic", alpha=args.alpha,
                            prompt_len=PROMPT_LEN, gen_len=args.gen_len, max_context=MAX_CTX,
                            target_seed=1, draft_seed=2, capacity=8192,
                            **bench_knobs(args))
@@ -347,7 +361,7 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
         raise SystemExit("bench: generate() stream differs from the greedy stream")
     rf = gemv_roofline(eng)
     # the CPU baseline is timed on rank 0 at N=1 only (the bench contract)
-    cpu = cpu_baseline() if not args.no_cpu and n_gpus == 1 else None
+    cpu = cpu_baseline(shape=args.target) if not args.no_cpu and n_gpus == 1 else None
     wb = eng.target.config.weight_bytes()
     return {
         "metric": "single-request generated tokens/s + inter-token latency",
@@ -356,12 +370,13 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
         "ms_per_step": round(total_s / args.steps * 1e3, 2),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, PCG64 prompts)",
-        "config": {"workload": "configs[1]: Llama-2-7B-shape target + 160M-shape draft, "
-                               f"bf16, async-speculative (PipeInfer), "
+        "config": {"workload": WORKLOADS.get((args.target, args.draft),
+                                             f"{args.target} target + {args.draft} draft")
+                               + f", bf16, async-speculative (PipeInfer), "
                                f"{eng.pipe.n_stages}-stage pipeline"
                                + (", dedicated draft GPU" if eng.pipe.n_stages < n_gpus
                                   else ", draft shares GPU 0"),
-                   "target": TARGET, "draft": DRAFT, "alpha": ALPHA,
+                   "target": args.target, "draft": args.draft, "alpha": args.alpha,
                    "prompt_len": PROMPT_LEN, "gen_len": args.gen_len,
                    "pipeline_stages": eng.pipe.n_stages,
                    "engine": {"microbatch": eng.cfg.microbatch, "partitions": eng.cfg.partitions,
@@ -370,14 +385,13 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
                               if os.environ.get("SP_DRAFT_FUSED", "1") != "0" else "per-forward",
                               "spec_ramp": eng.cfg.spec_ramp,
                               "continuous": eng.cfg.continuous,
-                              "fold_frontier": eng.last_head_policy.get("fold_frontier"),
-                              "max_inflight": eng.last_head_policy.get("max_inflight"),
+                              "head_policy": dict(eng.last_head_policy),
                               "draft_exclusive": eng.cfg.draft_exclusive,
                               "tree_width": eng.cfg.tree_width,
                               **({"alpha_sibling": eng.cfg.alpha_sibling}
                                  if eng.cfg.tree_width > 1 else {}),
                               **({"free_draft": True} if not eng.cfg.draft_charge else {})},
-                   "l2": "weights 13.2 GB >> 126 MB L2 (no flush needed)"},
+                   "l2": f"weights {wb / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"},
         "itl_ms": round(itl * 1e3, 3),
         "streams_checked": {"timed_steps": len(res), "sync": nb, "iterative": nb, "e2e": 1,
                             "equal_to_greedy": True,
@@ -410,10 +424,10 @@ def run_reference(args) -> dict:
         return None
     vals = []
     for _ in range(args.warmup):
-        cpu_baseline(n_decode=1)
+        cpu_baseline(n_decode=1, shape=args.target)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_baseline(n_decode=2))
+        vals.append(cpu_baseline(n_decode=2, shape=args.target))
     el = time.perf_counter() - t0
     v = statistics.median(x["value"] for x in vals)
     c = vals[0]
@@ -425,7 +439,7 @@ def run_reference(args) -> dict:
             "dtype": "f64", "data": "synthetic (random-init weights)", "impl": "reference",
             "config": {"workload": "configs[1]: Llama-2-7B-shape target (CPU reference "
                                    "algorithm, float64, one request)",
-                       "target": TARGET, "prompt_len": PROMPT_LEN},
+                       "target": args.target, "prompt_len": PROMPT_LEN},
             "itl_ms": round(1e3 / v, 1),
             "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": c["cores"],
                              "kind": "port", "sample": c["sample"]},
@@ -439,6 +453,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--gen-len", type=int, default=GEN_LEN)
+    ap.add_argument("--target", default=TARGET, help="target shape (model.LLAMA_SHAPES)")
+    ap.add_argument("--draft", default=DRAFT, help="draft shape (model.LLAMA_SHAPES)")
+    ap.add_argument("--alpha", type=float, default=ALPHA,
+                    help="synthetic draft acceptance (configs[3]: low alpha exercises "
+                         "early cancellation)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--node-weights", type=lambda v: tuple(float(x) for x in v.split(",")),

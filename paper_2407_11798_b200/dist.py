@@ -475,8 +475,8 @@ def bench_main(args):
         os.environ.setdefault("SP_DRAFT_FUSED", "1")
         os.environ.setdefault("SP_DRAFT_KERNEL", "grid")
     cfg = ExperimentConfig(mode="async-speculative", nodes=world if dedicated else world + 1,
-                           target_shape=B.TARGET, draft_shape=B.DRAFT,
-                           draft_backend="synthetic", alpha=B.ALPHA,
+                           target_shape=args.target, draft_shape=args.draft,
+                           draft_backend="synthetic", alpha=args.alpha,
                            prompt_len=B.PROMPT_LEN, gen_len=args.gen_len,
                            max_context=B.MAX_CTX, target_seed=1, draft_seed=2,
                            capacity=8192, node_weights=getattr(args, "node_weights", None),
