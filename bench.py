@@ -12,9 +12,11 @@ reference's generation speed (engine.py:1234-1243: accepted tokens after
 prefill / time from end of prefill to the last acceptance), aggregated over
 the K timed steps; ``itl_ms`` the mean inter-token latency.
 
-``--impl reference`` times the reference's CPU algorithm (the float64 oracle
-restatement, oracle/) on this host's cores on a bounded sample of the same
-workload (2 decoder layers at 7B width, extrapolated to 32 layers + head).
+``--impl reference`` times the reference's CPU implementation on this host's
+cores: the reference package itself when oracle/vendor_ref.sh has vendored
+it into oracle/_ref (its decoder at the target's width, 2 layers
+extrapolated to the target's depth + head; plus cfg1 reference_decode and
+the four modes under simulate(clock="wall")), else the float64 oracle port.
 """
 
 from __future__ import annotations
@@ -361,7 +363,11 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
         raise SystemExit("bench: generate() stream differs from the greedy stream")
     rf = gemv_roofline(eng)
     # the CPU baseline is timed on rank 0 at N=1 only (the bench contract)
-    cpu = cpu_baseline(shape=args.target) if not args.no_cpu and n_gpus == 1 else None
+    cpu = None
+    if not args.no_cpu and n_gpus == 1:
+        from oracle import reference_arm as R
+        cpu = (_reference_baseline(args.target, n_decode=2) if R.available()
+               else cpu_baseline(shape=args.target))
     wb = eng.target.config.weight_bytes()
     return {
         "metric": "single-request generated tokens/s + inter-token latency",
@@ -418,33 +424,78 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
     }
 
 
+def _reference_baseline(shape: str, n_decode: int) -> dict:
+    """The reference itself (oracle/_ref, vendored by oracle/vendor_ref.sh)
+    on this host's cores: its own decoder at the target's width, per-token
+    time extrapolated to the target's depth."""
+    import numpy  # noqa: F401  (BLAS loaded before threadpoolctl looks)
+    from oracle import reference_arm as R
+    from paper_2407_11798_b200.model import LLAMA_SHAPES
+    sh = LLAMA_SHAPES[shape]
+    sp = R.load()
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        with threadpool_limits(limits=os.cpu_count() or 1):
+            cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+            w = R.width_extrapolated(sp, sh["embed_dim"], sh["n_heads"], sh["n_layers"],
+                                     vocab=sh["vocab_size"], n_decode=n_decode,
+                                     layers=1 if sh["embed_dim"] >= 8192 else 2)
+    except ImportError:
+        cores = os.cpu_count() or 1
+        w = R.width_extrapolated(sp, sh["embed_dim"], sh["n_heads"], sh["n_layers"],
+                                 vocab=sh["vocab_size"], n_decode=n_decode)
+    return {"value": w["tokens_per_s"], "unit": "tokens/s", "cores": cores, "kind": "reference",
+            "sample": w["sample"], "ms_per_token": w["ms_per_token"],
+            "per_layer_ms": round(w["per_layer_ms"], 2), "head_ms": round(w["head_ms"], 2)}
+
+
 def run_reference(args) -> dict:
+    """The reference arm: the reference's CPU implementation of the path on
+    this host's cores (rank 0 only).  With oracle/_ref present that is the
+    reference package itself (kind "reference"): its decoder at the
+    target's width (the reference cannot run Llama; extrapolated), plus the
+    cfg1 figures BASELINE.md §3 asks for (reference_decode and the four
+    modes under simulate(clock="wall")).  Without it, the float64 oracle
+    port of the Llama forward (kind "port")."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
+    from oracle import reference_arm as R
+    use_ref = R.available()
     vals = []
-    for _ in range(args.warmup):
-        cpu_baseline(n_decode=1, shape=args.target)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(n_decode=2, shape=args.target))
+    if use_ref:
+        c = _reference_baseline(args.target, n_decode=max(1, args.steps))
+        vals = [c]
+        sp = R.load()
+        extra = {"reference_cfg1": {"setting": {**R.CFG1, "stages": 4, "alpha": 0.8,
+                                                "clock": "wall", "delays": 0},
+                                    "reference_decode": R.cfg1_decode(sp),
+                                    "simulate_wall": R.cfg1_modes(sp)}}
+    else:
+        for _ in range(args.warmup):
+            cpu_baseline(n_decode=1, shape=args.target)
+        for _ in range(args.steps):
+            vals.append(cpu_baseline(n_decode=2, shape=args.target))
+        extra = {}
     el = time.perf_counter() - t0
     v = statistics.median(x["value"] for x in vals)
     c = vals[0]
     return {"metric": "single-request generated tokens/s + inter-token latency",
             "value": round(v, 4), "unit": "tokens/s",
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 1),
+            "warmup": args.warmup, "ms_per_step": round(el / max(1, args.steps) * 1e3, 1),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (random-init weights)", "impl": "reference",
-            "config": {"workload": "configs[1]: Llama-2-7B-shape target (CPU reference "
-                                   "algorithm, float64, one request)",
+            "config": {"workload": WORKLOADS.get((args.target, args.draft),
+                                                 f"{args.target} target")
+                                   + " (CPU reference, float64, one request)",
                        "target": args.target, "prompt_len": PROMPT_LEN},
             "itl_ms": round(1e3 / v, 1),
             "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": c["cores"],
-                             "kind": "port", "sample": c["sample"]},
+                             "kind": c["kind"], "sample": c["sample"]},
             "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0}, **extra}
 
 
 def main():
