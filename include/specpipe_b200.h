@@ -332,6 +332,9 @@ int sp_stage_decode_chain_ok(const sp_stage* s);
 #define SP_DRAFT_KIND_CLUSTER 1
 #define SP_DRAFT_KIND_GRID 2
 int sp_stage_set_draft_kernel(sp_stage* s, int kind);
+/* Text of the last CUDA failure behind an SP_ERR_CUDA status on this thread
+ * ("runtime.cu:<line>: <call> -> <cudaGetErrorString>"), "" if none. */
+const char* sp_last_error(void);
 int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_feed, int pos0,
                           const int32_t* step_tokens, int steps, float cutoff,
                           sp_row_result* out, int* err_out, void* stream);

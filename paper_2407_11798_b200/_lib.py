@@ -112,6 +112,7 @@ PROTOTYPES = {
     "sp_stage_truncate": (I, [P, I]),
     "sp_stage_decode_chain_ok": (I, [P]),
     "sp_stage_set_draft_kernel": (I, [P, I]),
+    "sp_last_error": (C.c_char_p, []),
     "sp_stage_compact": (I, [P, P]),
     "sp_stage_draft_profile": (I, [P, P, I]),
     "sp_stage_chain_begin": (I, [P, F, P, P]),
@@ -180,7 +181,12 @@ def check(rc: int, what: str = "") -> None:
         raise CacheError(msg)
     if rc == SP_ERR_PROTOCOL:
         raise ProtocolError(msg)
-    raise RuntimeError(f"specpipe_b200 CUDA failure ({msg})")
+    detail = ""
+    try:
+        detail = (load().sp_last_error() or b"").decode(errors="replace")
+    except Exception:
+        pass
+    raise RuntimeError(f"specpipe_b200 CUDA failure ({msg}{': ' + detail if detail else ''})")
 
 
 def raise_device_error(bits: int, where: str = "") -> None:

@@ -171,12 +171,6 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
   pdl_trigger();
   if (a.diag_empty) return;   // diagnostics: kernel-boundary cost only
 
-  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 &&
-      a.cancel_word != nullptr && a.run_state_w != nullptr) {
-    // Early inference cancellation: observe the device-visible cancel word
-    // once per layer; every later kernel of this run reads run_state.
-    if (ld_volatile(a.cancel_word) == a.run_id) atomicExch(a.run_state_w, 1);
-  }
   if (run_skipped(a.run_state)) return;
 
   const int ns = (len + ATT_CH - 1) / ATT_CH;
@@ -376,10 +370,6 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_flat_kernel(const AttnArgs a
   extern __shared__ int32_t splan[];          // [len]
   __shared__ float gm[G], gl[G];
   __shared__ float gacc[G][HD];
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 &&
-      a.cancel_word != nullptr && a.run_state_w != nullptr) {
-    if (ld_volatile(a.cancel_word) == a.run_id) atomicExch(a.run_state_w, 1);
-  }
   if (run_skipped(a.run_state)) return;
   const int h = blockIdx.x, i = blockIdx.y;
   const int len = a.vis_len[i];
@@ -469,13 +459,12 @@ template <typename T, int HD>
 static cudaError_t launch_attn_flat(AttnArgs a, cudaStream_t st) {
   const size_t smem = sizeof(int32_t) * (size_t)a.ld_vis;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  if (smem > 48 * 1024) {
-    static size_t configured = 0;
-    if (configured < smem) {
-      cudaFuncSetAttribute(attn_flat_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      configured = smem;
-    }
+  static size_t configured = 0;
+  if (configured < smem) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        attn_flat_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
   }
   return launch_pdl(attn_flat_kernel<T, HD>, dim3(a.H, a.n), dim3(ATT_THREADS), smem, st, a);
 }
@@ -489,13 +478,14 @@ static cudaError_t launch_attn_hd(dim3 grid, AttnArgs a, cudaStream_t st) {
   if (flat && (size_t)a.ld_vis * 4 <= 200 * 1024) return launch_attn_flat<T, HD>(a, st);
   const size_t smem = sizeof(float) * (size_t)a.nsplit * (HD + 2);
   a.merge_smem = smem <= 96 * 1024 ? 1 : 0;
-  if (a.merge_smem && smem > 48 * 1024) {
-    static size_t configured = 0;
-    if (configured < smem) {
-      cudaFuncSetAttribute(attn_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           96 * 1024);
-      configured = 96 * 1024;
-    }
+  // (the 48 KB default covers static + dynamic shared memory together:
+  // raise the limit before the first launch that could cross it)
+  static bool configured = false;
+  if (a.merge_smem && !configured) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        attn_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
   }
   return launch_pdl(attn_kernel<T, HD>, grid, dim3(ATT_THREADS), a.merge_smem ? smem : 0, st, a);
 }
@@ -522,7 +512,7 @@ cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
                         const int* run_state, const RunHdr* hdr) {
   const size_t smem = (size_t)(max_context + 1) * sizeof(int);
   static int configured = 0;
-  if (smem > 48 * 1024 && configured < (int)smem) {
+  if (configured < (int)smem) {   // (48 KB default covers static + dynamic)
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     configured = (int)smem;
@@ -540,6 +530,7 @@ cudaError_t launch_attention(const AttnArgs& a0, int kv_dtype, int hd,
   if (nopre) { a.fresh_row0_dev = nullptr; a.fresh_row0 = 0; }
   if (diag == 2) return cudaSuccess;   // diagnostics: no attention launch at all
   a.diag_empty = diag == 1;
+  if (attn_tc_ok(kv_dtype, hd, a.n)) return launch_attention_tc(a, hd, st);
   return kv_dtype == SP_DTYPE_BF16 ? attn_dispatch<__nv_bfloat16>(a, hd, st)
                                    : attn_dispatch<float>(a, hd, st);
 }

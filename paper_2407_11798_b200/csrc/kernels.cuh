@@ -160,6 +160,9 @@ cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
 cudaError_t launch_attention(const AttnArgs& a, int kv_dtype, int hd,
                              cudaStream_t st);
 int attn_splits(int max_len);
+// tensor-core attention over bf16 caches (attention_tc.cu)
+bool attn_tc_ok(int kv_dtype, int hd, int n);
+cudaError_t launch_attention_tc(const AttnArgs& a, int hd, cudaStream_t st);
 cudaError_t launch_lmhead(const LmArgs& a, int w_dtype, cudaStream_t st);
 int lmhead_grid(int V);
 cudaError_t launch_meta_write(int32_t* pos, uint32_t* mask, int row0,

@@ -159,7 +159,7 @@ cudaError_t launch_copy(const int32_t* pos, uint32_t* mask, int n, int src,
   if (n <= 0) return cudaSuccess;
   const size_t smem = (size_t)max_context * sizeof(uint32_t);
   static size_t configured = 0;
-  if (smem > 48 * 1024 && configured < smem) {
+  if (configured < smem) {   // (48 KB default covers static + dynamic)
     cudaFuncSetAttribute(copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     configured = smem;

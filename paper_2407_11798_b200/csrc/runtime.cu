@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include <cstdio>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -356,10 +357,21 @@ struct sp_stage {
 };
 
 static int cuda_status(cudaError_t e) { return e == cudaSuccess ? SP_OK : SP_ERR_CUDA; }
-#define SP_CHECK(call)                       \
-  do {                                       \
-    cudaError_t _e = (call);                 \
-    if (_e != cudaSuccess) return SP_ERR_CUDA; \
+// the first failing call of the last failed entry point, for sp_last_error()
+static thread_local char g_last_error[320];
+static void note_cuda_error(cudaError_t e, const char* what, int line) {
+  snprintf(g_last_error, sizeof(g_last_error), "runtime.cu:%d: %s -> %s", line, what,
+           cudaGetErrorString(e));
+}
+extern "C" const char* sp_last_error(void) { return g_last_error; }
+
+#define SP_CHECK(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) {                             \
+      note_cuda_error(_e, #call, __LINE__);              \
+      return SP_ERR_CUDA;                                \
+    }                                                    \
   } while (0)
 
 static size_t wbytes(const sp_model_dims& d) { return d.w_dtype == SP_DTYPE_BF16 ? 2 : 4; }
@@ -965,6 +977,14 @@ static int check_run(sp_stage* s, const sp_token* toks, int n, int layer_a, int 
   if (layer_a > 0 && !x_in) return SP_ERR_MODEL;  // model.py:361-362
   for (int l = layer_a; l < layer_b; ++l)
     if (!s->layers[l - s->lo].qkv) return SP_ERR_ARG;
+  // host-visible token ids and positions are rejected eagerly (the device
+  // checks stay for chain-fed tokens): an out-of-range position would index
+  // past the RoPE / cache tables before the sticky error is read
+  if (toks)
+    for (int i = 0; i < n; ++i)
+      if (toks[i].pos < 0 || toks[i].pos >= s->dims.max_context || toks[i].token < 0 ||
+          toks[i].token >= s->dims.vocab)
+        return SP_ERR_MODEL;
   return SP_OK;
 }
 

@@ -13,9 +13,10 @@ import paper_2407_11798_b200 as sp
 from paper_2407_11798_b200.model import BatchToken, encode_tokens
 from paper_2407_11798_b200.pipeline import LocalPipeline
 
-cfg = sp.llama_config("llama2-7b")
+ctx_arg = int(sys.argv[1]) if len(sys.argv) > 1 else 384
+cfg = sp.llama_config("llama2-7b", max_context=max(1024, ctx_arg + 64))
 m = sp.build_model(cfg, torch.device("cuda", 0))
-pipe = LocalPipeline(m, [(0, 32)], partitions=8, capacity=4096, max_tokens=256)
+pipe = LocalPipeline(m, [(0, 32)], partitions=8, capacity=max(4096, ctx_arg + 256), max_tokens=256)
 ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 384
 pre = [BatchToken(5 + (i % 100), i, frozenset([0]), i == ctx - 1) for i in range(ctx)]
 for c0 in range(0, ctx, 128):
