@@ -477,7 +477,8 @@ static cudaError_t launch_attn_hd(dim3 grid, AttnArgs a, cudaStream_t st) {
   static const bool flat = getenv("SP_ATTN_FLAT") != nullptr;
   if (flat && (size_t)a.ld_vis * 4 <= 200 * 1024) return launch_attn_flat<T, HD>(a, st);
   const size_t smem = sizeof(float) * (size_t)a.nsplit * (HD + 2);
-  a.merge_smem = smem <= 96 * 1024 ? 1 : 0;
+  static const int msm = getenv("SP_ATT_MERGE_SMEM_KB") ? atoi(getenv("SP_ATT_MERGE_SMEM_KB")) : 96;
+  a.merge_smem = smem <= (size_t)msm * 1024 ? 1 : 0;
   // (the 48 KB default covers static + dynamic shared memory together:
   // raise the limit before the first launch that could cross it)
   static bool configured = false;
@@ -492,8 +493,11 @@ static cudaError_t launch_attn_hd(dim3 grid, AttnArgs a, cudaStream_t st) {
 
 template <typename T>
 static cudaError_t attn_dispatch(const AttnArgs& a, int hd, cudaStream_t st) {
-  // about 4 CTAs per SM in total; splits beyond gridDim.z loop in-CTA
-  const int want = (4 * 148 + a.H * a.n - 1) / (a.H * a.n);
+  // a few CTAs per SM in total; splits beyond gridDim.z loop in-CTA
+  // (8 per SM measured best on the 7B decode: ctx 640 11.8 -> 9.4 us; the
+  // split partition is by plan index, so the grid never changes the bits)
+  static const int per_sm = getenv("SP_ATT_CTAS_PER_SM") ? atoi(getenv("SP_ATT_CTAS_PER_SM")) : 8;
+  const int want = (per_sm * 148 + a.H * a.n - 1) / (a.H * a.n);
   const dim3 grid(a.H, a.n, max(1, min(a.nsplit, want)));
   switch (hd) {
     case 8: return launch_attn_hd<T, 8>(grid, a, st);

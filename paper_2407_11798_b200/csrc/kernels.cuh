@@ -53,6 +53,12 @@ struct AttnArgs {
   const int32_t* fresh_row0_dev;
   int fresh_row0;
   int diag_empty;   // diagnostics only (SP_ATT_DIAG=1): return after the dependency wait
+  // the run's tokens and header (tensor-core kernel: in a run whose
+  // coverage is checked -- every token sees exactly one cell per earlier
+  // position -- a query on the reference query's sequence set has a plan
+  // that is a prefix of the reference's), or null
+  const sp_token* toks;
+  const RunHdr* hdr;
 };
 
 struct LmPartial {

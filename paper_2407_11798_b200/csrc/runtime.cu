@@ -825,6 +825,8 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     a.run_state = s->run_state; a.run_state_w = nullptr;
     a.cancel_word = nullptr; a.run_id = 0; a.err = s->err;
     a.fresh_row0_dev = row0_dev;   // the QKV epilogue writes rows row0 .. row0 + n
+    a.toks = s->hdr_toks;
+    a.hdr = (const RunHdr*)s->hdr;
     if (s->tc) {
       // ---- tensor-core path (tcgen05, bf16 activations, fp32 accumulate) ----
       TcArgs t{};
