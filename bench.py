@@ -21,6 +21,7 @@ the four modes under simulate(clock="wall")), else the float64 oracle port.
 
 from __future__ import annotations
 
+from typing import Optional
 import argparse
 import json
 import os
@@ -204,7 +205,7 @@ def gemv_roofline(engine, reps: int = 5) -> dict:
     out = torch.zeros((256, 2 * f + q + 2 * kv), device=dev, dtype=torch.float32)
     scratch = torch.zeros(8 << 20, device=dev)
     tick = torch.zeros(4096, dtype=torch.int32, device=dev)
-    args, nbytes = [], 0
+    args, nbytes, kinds = [], 0, []
     for l in layers:
         L = engine.target.layers[l]
         for key, n, k in (("qkv", q + 2 * kv, d), ("o", d, q), ("up", 2 * f, d),
@@ -214,6 +215,7 @@ def gemv_roofline(engine, reps: int = 5) -> dict:
             a.out, a.ldo = out.data_ptr(), out.shape[1]
             a.scratch, a.tickets = scratch.data_ptr(), tick.data_ptr()
             args.append(a)
+            kinds.append((key, n * k * 2 + 2 * k + 4 * n))
             nbytes += n * k * 2 + 2 * k + 4 * n
     s = torch.cuda.Stream(dev)
     graph = torch.cuda.CUDAGraph()
@@ -236,6 +238,28 @@ def gemv_roofline(engine, reps: int = 5) -> dict:
     t = statistics.median(times)
     peak, how = _peaks()
     achieved = nbytes / t / 1e9
+    # per matrix kind: the same launches, one kind per graph
+    per = {}
+    for kind in ("qkv", "o", "up", "down"):
+        sel = [a for a, (k_, _) in zip(args, kinds) if k_ == kind]
+        byt = sum(b for k_, b in kinds if k_ == kind)
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=s):
+            for a in sel:
+                _lib.check(lib.sp_tc_gemm(C.byref(a), X.data_ptr(), 256, s.cuda_stream))
+        ts = []
+        for rep in range(reps + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                e0.record(s)
+                g2.replay()
+                e1.record(s)
+            e1.synchronize()
+            if rep:
+                ts.append(e0.elapsed_time(e1) / 1e3)
+        tk = statistics.median(ts)
+        per[kind] = {"us_per_launch": round(tk / len(sel) * 1e6, 2),
+                     "achieved": round(byt / tk / 1e9, 1), "frac": round(byt / tk / 1e9 / peak, 4)}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
     if os.path.exists(tp):
@@ -243,11 +267,67 @@ def gemv_roofline(engine, reps: int = 5) -> dict:
             traffic = json.load(fh).get("bytes_per_launch")
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
             "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_source": "static: ncu --set full capture of the same GEMM replay, "
+                              "profiles/ncu_gemm_traffic.json (dram read+write per launch)",
+            "per_matrix": per,
             "kernel": "tc_gemm_kernel<NT=16> (tcgen05+TMEM, bulk-copied tiled bf16 "
                       "weights; QKV+O+gate/up+down of every layer of the stage, M=1)",
             "algorithmic_bytes_per_launch": round(nbytes / len(args)),
             "avg_launch_us": round(t / len(args) * 1e6, 2), "launches": len(args),
             "peak_source": how}
+
+
+def stage_run_roofline(eng, peak: float, runs: int = 24) -> Optional[dict]:
+    """In-context roofline of the product path: back-to-back 1-token decode
+    stage-runs through the engine's own pipeline (graph-replayed
+    sp_stage_step: fused QKV/RoPE, attention, residual and SwiGLU epilogues,
+    fused LM head), timed with CUDA events on the stage stream after a
+    128-token prefill.  Algorithmic bytes per run = every weight byte of the
+    stage (+ LM head) + the K/V rows read; achieved = bytes / run time."""
+    import torch
+    import paper_2407_11798_b200 as sp
+    from paper_2407_11798_b200.model import BatchToken, encode_tokens
+    pipe = eng.pipe
+    if not hasattr(pipe, "stream") or not getattr(pipe, "stages", None):
+        return None            # (the distributed pipeline: workers hold the stages)
+    cfg = eng.target.config
+    pipe.reset()
+    prompt = sp.sample_prompt(7, PROMPT_LEN, cfg.vocab_size)
+    pre = [BatchToken(t, i, frozenset([0]), i == PROMPT_LEN - 1) for i, t in enumerate(prompt)]
+    pipe.launch(1, sp.model.KIND_CODE[sp.PREFILL], encode_tokens(pre), 0, [PROMPT_LEN - 1])
+    pipe.wait()
+
+    def decode(rid, pos):
+        b = [BatchToken(int(prompt[pos % PROMPT_LEN]), pos, frozenset([0]), True)]
+        pipe.launch(rid, sp.model.KIND_CODE[sp.NON_SPECULATIVE], encode_tokens(b), 0, [0])
+    for i in range(4):         # capture / warm the 1-token graph
+        decode(2 + i, PROMPT_LEN + i)
+        pipe.wait()
+    st = pipe.stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    base = PROMPT_LEN + 4
+    for i in range(runs):
+        decode(100 + i, base + i)
+    e1.record(st)
+    for _ in range(runs):
+        pipe.wait()
+    e1.synchronize()
+    t = e0.elapsed_time(e1) / 1e3 / runs
+    pipe.reset()
+    layers = sum(st_.hi - st_.lo for st_ in pipe.stages)
+    head = any(st_.hi == cfg.n_layers for st_ in pipe.stages)
+    wb = cfg.weight_bytes(layers=layers, head=head)
+    ctx = base + runs // 2
+    kvb = layers * ctx * cfg.kv_dim * 2 * (4 if cfg.weight_dtype == "fp32" else 2)
+    ach = (wb + kvb) / t / 1e9
+    return {"ms_per_run": round(t * 1e3, 4), "layers": layers, "lm_head": head,
+            "algorithmic_bytes_per_run": wb + kvb, "achieved": round(ach, 1),
+            "frac": round(ach / peak, 4),
+            "note": "1-token decode stage-runs back to back through the product path "
+                    f"(graph replay, context {base}..{base + runs}), CUDA events on the "
+                    "stage stream"}
 
 
 # ---------------------------------------------------------------------------
@@ -362,6 +442,7 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
     if out != eng._tables[tuple(prompt)][0][PROMPT_LEN:PROMPT_LEN + len(out)]:
         raise SystemExit("bench: generate() stream differs from the greedy stream")
     rf = gemv_roofline(eng)
+    rf["stage_run"] = stage_run_roofline(eng, rf["peak"])
     # the CPU baseline is timed on rank 0 at N=1 only (the bench contract)
     cpu = None
     if not args.no_cpu and n_gpus == 1:
