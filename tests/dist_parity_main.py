@@ -33,12 +33,14 @@ def _cases():
     ref = ExperimentConfig(mode="async-speculative", vocab_size=256, embed_dim=64,
                            target_layers=8, n_heads=2, draft_layers=1, max_context=256,
                            prompt_len=PROMPT, gen_len=GEN, target_seed=3, draft_seed=4,
-                           draft_backend="synthetic", alpha=0.6, capacity=2048)
+                           draft_backend="synthetic", alpha=0.6, capacity=2048,
+                           partitions=16)
     llama = ExperimentConfig(mode="async-speculative", arch="llama", vocab_size=512,
                              embed_dim=256, target_layers=8, n_heads=4, draft_layers=1,
                              draft_embed_dim=256, max_context=256, prompt_len=PROMPT,
                              gen_len=GEN, target_seed=5, draft_seed=6,
-                             draft_backend="synthetic", alpha=0.6, capacity=2048)
+                             draft_backend="synthetic", alpha=0.6, capacity=2048,
+                             partitions=16)
     return {"ref": ref, "llama": llama}
 
 
@@ -95,6 +97,11 @@ def main(out_path):
                     r = eng.run(prompt=list(prompt), mode=mode)
                     got[mode] = r.tokens
                     got[mode + ":cancelled"] = r.metrics.cancelled_runs
+                # tree speculation (runner-up siblings on their own partitions)
+                eng.cfg = replace(cfg, tree_width=2, alpha_sibling=0.6)
+                for mode in ("async-speculative", "sync-speculative"):
+                    got[mode + ":tree"] = eng.run(prompt=list(prompt), mode=mode).tokens
+                eng.cfg = cfg
                 results[f"{name}/{layout}"] = got
                 pipe.shutdown()
                 del eng, pipe, draft

@@ -1,7 +1,8 @@
 """Multi-GPU parity (VERDICT r01 "Next round" 2): the NCCL
 pipeline's token streams at N GPUs equal the oracle (fp32 toy decoder) and
 the 1-GPU stream (bf16 llama), in the async, sync and pipeline-iterative
-modes and in both layouts.  Needs >= 2 GPUs (``gpurun --gpus 2``); on a
+modes (and the two speculative modes with tree speculation) and in both
+layouts.  Needs >= 2 GPUs (``gpurun --gpus 2``); on a
 1-GPU box it skips.  The world size is every visible GPU, capped at 4."""
 
 import json
@@ -41,5 +42,6 @@ def test_multi_gpu_streams_match(tmp_path):
     assert d["world"] == n
     for case, got in d["results"].items():
         want = d["refs"][case.split("/")[0]]
-        for mode in ("async-speculative", "sync-speculative", "pipeline-iterative"):
+        for mode in ("async-speculative", "sync-speculative", "pipeline-iterative",
+                     "async-speculative:tree", "sync-speculative:tree"):
             assert got[mode] == want, (case, mode)
