@@ -73,6 +73,11 @@ class _DraftBase:
         self.rows_host = torch.zeros((66, 4), dtype=torch.int32).pin_memory()
         self.event = torch.cuda.Event()
         self.tokens: List[int] = []
+        # tokens [0, cached) have K/V cells; the persistent kernels do not
+        # forward a request's LAST proposal (only the next request needs its
+        # cells, and feeds it then in the same forward as its own tokens:
+        # one draft forward per request saved)
+        self.cached = 0
         self.seconds: tuple = ()   # the draft's runner-up per proposal (tree speculation)
         self._pending = None
         self.forwards = 0          # draft-model forwards issued (cost accounting)
@@ -90,16 +95,21 @@ class _DraftBase:
             self.reply()
         self.stage.reset()
         self.tokens = []
+        self.cached = 0
         self.stream.synchronize()
 
     # -- shared GPU steps -------------------------------------------------------
     def _truncate(self, n: int) -> None:
         """Rows == positions: drop tokens >= n and every cell past the kept
-        tokens (dead chain steps included)."""
+        tokens (dead chain steps and a not-yet-forwarded proposal included)."""
         if n < len(self.tokens):
             self.stage.invalidate_tip()
             del self.tokens[n:]
-        self.stage.truncate(len(self.tokens))
+        if self.cached > len(self.tokens):
+            self.cached = len(self.tokens)
+        elif self.cached < len(self.tokens):
+            self.stage.invalidate_tip()      # the tip predates the uncached token
+        self.stage.truncate(self.cached)
 
     def _launch_chain(self, feed: Sequence[int], pos0: int, steps: int, cutoff: float,
                       step_tokens: Optional[Sequence[int]] = None) -> None:
@@ -206,16 +216,25 @@ class ModelDraftServer(_DraftBase):
         budget = max(0, min(int(max_tokens), room, 4))
         c32 = float(np.float32(cutoff))
         if self.fused:
-            if feed or budget > 0:
-                self._chain(feed, budget, c32)
+            # uncached kept tokens ride in front of this request's feed; the
+            # chain runs budget - 1 steps (the last proposal is not forwarded)
+            full = self.tokens[self.cached:] + feed
+            if full or budget > 0:
+                self._launch_chain(full, self.cached, max(0, budget - 1), c32)
             else:
                 self.event.record(self.stream)
+            self.tokens.extend(feed)
+            self.cached = len(self.tokens)
             self._pending = (budget, np.float32(cutoff), True)
-            self._mark_end(len(feed), budget)
+            self._mark_end(len(full), budget)
             return
+        if self.cached < len(self.tokens):        # (a kernel-path leftover)
+            feed = self.tokens[self.cached:] + feed
+            del self.tokens[self.cached:]
         if feed:
             self._forward(feed, len(self.tokens))
             self.tokens.extend(feed)
+            self.cached = len(self.tokens)
         if budget > 0:
             self.stage.chain_begin(c32, self.res[0, 1].data_ptr())
             base = len(self.tokens)
@@ -250,6 +269,10 @@ class ModelDraftServer(_DraftBase):
             toks.append(int(r[j]["a"]))
             confs.append(float(conf))
             secs.append(int(r[j]["b"]))
+        # fused: proposals 1 .. budget-1 were forwarded (a proposal is fed
+        # only while the gate is open, i.e. when it was returned)
+        fed = min(len(toks), budget - 1) if fused else len(toks)
+        self.cached = len(self.tokens) + fed
         self.tokens.extend(toks)
         self.seconds = tuple(secs)
         return tuple(toks), tuple(confs)
@@ -301,12 +324,15 @@ class TableDraftServer(_DraftBase):
                 del self.tokens[truncate_to:]
             self.on_path = min(self.on_path, truncate_to)
         elif self.charge:
-            self.stage.truncate(len(self.tokens))
+            self._truncate(len(self.tokens))
         feed = list(feed)
         feed_pos = len(self.tokens)
+        pend = self.tokens[self.cached:] if self.charge else []   # kept, not yet forwarded
         if feed:
             if self.charge and not self.fused:
-                self._forward(feed, feed_pos)
+                self._forward(pend + feed, self.cached)
+                pend = []
+                self.cached = feed_pos + len(feed)
             self.tokens.extend(feed)
             self._retrack(feed_pos)
         room = self.max_context - len(self.tokens)
@@ -337,16 +363,27 @@ class TableDraftServer(_DraftBase):
                             alt = (best + 2) % self.vocab
                     secs.append(alt)
                 if self.charge and not self.fused:
-                    self._forward([tok], p)
+                    self._forward(pend + [tok], self.cached)
+                    pend = []
+                    self.cached = p + 1
                 self.tokens.append(tok)
                 self._retrack(p)
                 props.append(tok)
         self.seconds = tuple(secs)
         if self.charge and self.fused and (feed or props):
-            # the forwards a real draft would run, as one persistent launch
-            self._launch_chain(feed, feed_pos, len(props), 0.0, step_tokens=props)
-            self._pending = (tuple(props), True)
-            self._mark_end(len(feed), len(props))
+            # the forwards a real draft would run, as one persistent launch:
+            # kept-but-unforwarded tokens and the feed in one forward, then
+            # every proposal but the last (the next request forwards it)
+            full = pend + feed
+            steps = max(0, len(props) - 1)
+            if full or steps:
+                self._launch_chain(full, self.cached, steps, 0.0, step_tokens=props[:steps])
+                self.cached = feed_pos + len(feed) + steps
+                self._pending = (tuple(props), True)
+            else:
+                self._finish_enqueue(1)
+                self._pending = (tuple(props), False)
+            self._mark_end(len(full), len(props))
             return
         self._finish_enqueue(1)
         self._pending = (tuple(props), False)
