@@ -113,6 +113,7 @@ PROTOTYPES = {
     "sp_stage_decode_chain_ok": (I, [P]),
     "sp_stage_set_draft_kernel": (I, [P, I]),
     "sp_last_error": (C.c_char_p, []),
+    "sp_stage_set_skip_graphs": (I, [P, I]),
     "sp_stage_compact": (I, [P, P]),
     "sp_stage_draft_profile": (I, [P, P, I]),
     "sp_stage_chain_begin": (I, [P, F, P, P]),

@@ -1615,6 +1615,17 @@ extern "C" int sp_stage_decode_chain(sp_stage* s, const int32_t* feed, int n_fee
   return SP_OK;
 }
 
+extern "C" int sp_stage_set_skip_graphs(sp_stage* s, int on) {
+  if (!s) return SP_ERR_ARG;
+  const bool want = on != 0 && getenv("SP_NO_COND_GRAPH") == nullptr;
+  if (want != s->use_cond) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return SP_ERR_CUDA;
+    drop_graphs(s);     // captured steps hold the other structure
+    s->use_cond = want;
+  }
+  return SP_OK;
+}
+
 extern "C" int sp_stage_set_draft_kernel(sp_stage* s, int kind) {
   if (!s || kind < SP_DRAFT_KIND_AUTO || kind > SP_DRAFT_KIND_GRID) return SP_ERR_ARG;
   s->draft_kernel = kind;

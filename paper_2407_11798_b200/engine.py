@@ -1186,6 +1186,12 @@ class Engine:
         draft = self._make_draft(prompt, seed)
         wall0 = time.perf_counter()
         head = Head(cfg, self.pipe, draft, prompt, self.target.config.embed_dim)
+        # only an async head that can launch skippable runs needs the
+        # conditional (skip) graph bodies; they cost every full run ~0.1 ms
+        cancellable = cfg.mode == "async-speculative" and not (
+            head.fold_frontier and head.max_inflight == 1 and not head.adaptive)
+        if hasattr(self.pipe, "set_skip_graphs"):
+            self.pipe.set_skip_graphs(cancellable)
         runner = {"iterative": head.run_iterative,
                   "pipeline-iterative": head.run_iterative,
                   "sync-speculative": head.run_sync_speculative,

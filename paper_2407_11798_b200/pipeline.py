@@ -130,6 +130,14 @@ class LocalPipeline:
             self.timeline.append((run_id, kind, n, ev[0], ev[1]))
         self.fifo.append((run_id, slot, len(rows)))
 
+    def set_skip_graphs(self, on: bool) -> None:
+        """Conditional graph bodies only where runs can be cancelled."""
+        if getattr(self, "_skip_graphs", None) is not on:
+            self.stream.synchronize()
+            for st in self.stages:
+                st.set_skip_graphs(on)
+            self._skip_graphs = on
+
     def copy(self, src: int, dsts, end_pos: int) -> None:
         for st in self.stages:
             st.cache_copy(src, dsts, end_pos)

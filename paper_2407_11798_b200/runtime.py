@@ -157,6 +157,11 @@ class Stage:
             check(-rc, "sp_stage_compact")
         return rc
 
+    def set_skip_graphs(self, on: bool) -> None:
+        """Conditional (IF) graph bodies for cancellable stage-runs (see
+        sp_stage_set_skip_graphs)."""
+        check(self.lib.sp_stage_set_skip_graphs(self.h, 1 if on else 0), "sp_stage_set_skip_graphs")
+
     def truncate(self, n_cells: int) -> None:
         check(self.lib.sp_stage_truncate(self.h, int(n_cells)), "sp_stage_truncate")
 
