@@ -68,6 +68,8 @@ from .engine import (  # noqa: F401
     token_checksum,
 )
 
+from . import report  # noqa: F401,E402  (reference bench.py's report contract)
+
 LayeredModel = DeviceModel
 
 __version__ = "0.1.0"

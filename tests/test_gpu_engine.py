@@ -293,3 +293,23 @@ def test_tree_speculation_llama_deep(sp):
                                alpha=0.5, tree_width=2, alpha_sibling=0.6, partitions=16,
                                gen_len=48))
         assert res.tokens == it, mode
+
+
+def test_report_contract_on_gpu(sp, tmp_path, golden):
+    """run_experiment -> export -> load_report round trip, and the compare
+    command's verdict across all four modes (reference bench.py / cli.py)."""
+    from dataclasses import replace
+    from paper_2407_11798_b200 import report as R
+    base = cfg(sp, repetitions=2, draft_backend="synthetic", alpha=0.6)
+    reps = [R.run_experiment(replace(base, mode=m, nodes=n))
+            for m, n in (("iterative", 1), ("pipeline-iterative", 3),
+                         ("sync-speculative", 4), ("async-speculative", 4))]
+    assert reps[0].tokens[0] == _golden_stream(golden, 5)
+    code, detail = R.compare_exit_code(reps)
+    assert code == 0, detail
+    p = tmp_path / "rep.json"
+    R.export(reps[3], "json", str(p))
+    back = R.load_report(str(p))
+    assert back.checksum() == reps[3].checksum() and back.tokens == reps[3].tokens
+    R.export(reps[3], "csv", str(tmp_path / "rep.csv"))
+    assert all(R.consistency_gap(m) < 0.01 for m in reps[3].runs)
