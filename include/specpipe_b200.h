@@ -123,7 +123,10 @@ enum {
   SP_EPI_RESID = 1,   /* out += x @ W^T (+ finite check)   model.py:416,418 */
   SP_EPI_QKV = 2,     /* q -> out; k,v -> cache rows (+RoPE) model.py:387-393 */
   SP_EPI_GELU = 3,    /* out = gelu(norm(x) @ W^T)          model.py:417-418 */
-  SP_EPI_SWIGLU = 4   /* out = silu(g)*u, rows interleaved (g,u)            */
+  SP_EPI_SWIGLU = 4,  /* out = silu(g)*u, rows interleaved (g,u)            */
+  SP_EPI_LMHEAD = 5   /* greedy head: per token argmax / second / max-softmax
+                         over all rows (tile partials + a fixed-order merge);
+                         logits to out when out != NULL   model.py:424-457  */
 };
 
 typedef struct sp_gemv_args {
@@ -206,6 +209,17 @@ typedef struct sp_tc_args {
   int* err;
   const int* run_state;
   const int32_t* cache_row0_dev;  /* if set, overrides cache_row0 (run header) */
+  /* SP_EPI_LMHEAD (tensor-core LM head) */
+  sp_row_result* lm_out;   /* [m] records (argmax, second, conf, max logit) */
+  void* lm_part;           /* >= m * n_rows/128 partials of 32 bytes        */
+  int* lm_ticket;          /* zero-initialised; reset by the merging CTA    */
+  int* lm_err_out;         /* *err copied here when the head finishes       */
+  int* lm_status_out;      /* SP_STATUS_VALID, or PLACEHOLDER when skipped  */
+  int* lm_tip;             /* [argmax, conf bits, valid] of the last row    */
+  int* lm_gate;            /* chain gate (conf >= cutoff), with lm_chain_gate */
+  int32_t lm_chain_gate;
+  float lm_cutoff;
+  const void* lm_hdr;      /* run header (its cutoff wins when set)         */
 } sp_tc_args;
 
 /* Low-level form (tests): a->w tiled bf16; X bf16 [x_rows, k] row-major
@@ -260,6 +274,12 @@ int sp_stage_set_layer(sp_stage* s, int layer, const void* w_qkv,
                        const void* w_o, const void* w_up, const void* w_down,
                        const float* attn_norm, const float* mlp_norm);
 int sp_stage_set_head(sp_stage* s, const void* w_out, const float* final_norm);
+/* The LM head in the tensor-core tiled layout (model.tile_weight of w_out,
+ * vocab % 128 == 0): graph-replayed steps of a tiled stage then run the
+ * head as one tcgen05 GEMM with the fused greedy epilogue (SP_EPI_LMHEAD),
+ * flat in the number of rows up to 16 (the CUDA-core head re-streams per
+ * 8-row tile).  NULL restores the CUDA-core head. */
+int sp_stage_set_head_tiled(sp_stage* s, const void* w_out_tiled);
 /* device-visible cancel words: table[run_id % size] == run_id => cancelled */
 int sp_stage_set_cancel_table(sp_stage* s, const int* table, int size);
 /* CTA budget of this stage's tensor-core GEMMs (0 = whole GPU). */

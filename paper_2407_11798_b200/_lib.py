@@ -26,7 +26,7 @@ SP_DTYPE_F32, SP_DTYPE_BF16 = 0, 1
 SP_KIND_PREFILL, SP_KIND_NONSPEC, SP_KIND_SPEC = 0, 1, 2
 SP_STATUS_VALID, SP_STATUS_PLACEHOLDER = 0, 1
 SP_FWD_CHECK_COVERAGE, SP_FWD_SKIPPABLE, SP_FWD_CONTINUE, SP_FWD_CHAIN = 1, 2, 4, 8
-SP_EPI_STORE, SP_EPI_RESID, SP_EPI_QKV, SP_EPI_GELU, SP_EPI_SWIGLU = range(5)
+SP_EPI_STORE, SP_EPI_RESID, SP_EPI_QKV, SP_EPI_GELU, SP_EPI_SWIGLU, SP_EPI_LMHEAD = range(6)
 SP_STEP_TIP, SP_STEP_CHAIN = 1, 2
 SP_DRAFT_KIND_AUTO, SP_DRAFT_KIND_CLUSTER, SP_DRAFT_KIND_GRID = 0, 1, 2
 SP_LAYOUT_NATURAL, SP_LAYOUT_TC_TILED, SP_LAYOUT_SWZ8 = 0, 1, 2
@@ -76,7 +76,11 @@ class sp_tc_args(C.Structure):
                 ("xb_next", C.c_void_p), ("gain_next", C.c_void_p), ("scratch", C.c_void_p),
                 ("tickets", C.c_void_p), ("ksplit", C.c_int32), ("max_ctas", C.c_int32),
                 ("err", C.c_void_p),
-                ("run_state", C.c_void_p), ("cache_row0_dev", C.c_void_p)]
+                ("run_state", C.c_void_p), ("cache_row0_dev", C.c_void_p),
+                ("lm_out", C.c_void_p), ("lm_part", C.c_void_p), ("lm_ticket", C.c_void_p),
+                ("lm_err_out", C.c_void_p), ("lm_status_out", C.c_void_p),
+                ("lm_tip", C.c_void_p), ("lm_gate", C.c_void_p), ("lm_chain_gate", C.c_int32),
+                ("lm_cutoff", C.c_float), ("lm_hdr", C.c_void_p)]
 
 
 P = C.c_void_p
@@ -101,6 +105,7 @@ PROTOTYPES = {
     "sp_stage_set_embedding": (I, [P, P, P]),
     "sp_stage_set_layer": (I, [P, I, P, P, P, P, P, P]),
     "sp_stage_set_head": (I, [P, P, P]),
+    "sp_stage_set_head_tiled": (I, [P, P]),
     "sp_stage_set_cancel_table": (I, [P, P, I]),
     "sp_stage_set_cta_budget": (I, [P, I]),
     "sp_stage_forward": (I, [P, P, I, I, I, I, P, P, P, P, I, P]),

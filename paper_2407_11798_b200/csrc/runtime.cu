@@ -167,13 +167,14 @@ __global__ void gather_rows_kernel(const float* __restrict__ x, int d,
 // x (fixed-order block reduction) and the bf16 normed-input row x * gain.
 __global__ void prep_kernel(const float* __restrict__ x, int d,
                             const float* __restrict__ gain, __nv_bfloat16* __restrict__ xb,
-                            float* __restrict__ ss, const int* run_state) {
+                            float* __restrict__ ss, const int* run_state,
+                            const int32_t* __restrict__ rows) {
   pdl_wait();
   pdl_trigger();
   __shared__ float red[8];
   if (run_skipped(run_state)) return;
   const int t = blockIdx.x;
-  const float* xr = x + (size_t)t * d;
+  const float* xr = x + (size_t)(rows ? rows[t] : t) * d;   // (rows: the LM head's gather)
   float s = 0.f;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     const float v = xr[c];
@@ -264,6 +265,7 @@ struct sp_stage {
   const void* emb = nullptr;
   const float* pos_table = nullptr;
   const void* w_out = nullptr;
+  const void* w_out_tc = nullptr;        // tiled LM head (tensor-core head)
   const float* final_norm = nullptr;
   const int* cancel_table = nullptr;
   int cancel_size = 0;
@@ -535,6 +537,18 @@ extern "C" int sp_stage_set_head(sp_stage* s, const void* w_out,
   return SP_OK;
 }
 
+static void drop_graphs(sp_stage* s);
+
+extern "C" int sp_stage_set_head_tiled(sp_stage* s, const void* w_out_tiled) {
+  if (!s) return SP_ERR_ARG;
+  if (w_out_tiled && (!s->tc || s->dims.vocab % 128 || s->dims.d_model % 64 ||
+                      s->dims.w_dtype != SP_DTYPE_BF16))
+    return SP_ERR_ARG;
+  if (w_out_tiled != s->w_out_tc) drop_graphs(s);   // captured heads hold the other path
+  s->w_out_tc = w_out_tiled;
+  return SP_OK;
+}
+
 static void drop_graphs(sp_stage* s) {
   for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
   s->graphs.clear();
@@ -779,7 +793,7 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     // bf16 normed input of layer_a's attention norm + its statistic
     SP_CHECK(launch_pdl(prep_kernel, dim3(n), dim3(256), 0, st, (const float*)x_out, d,
                         s->layers[layer_a - s->lo].attn_norm, s->xb, s->ss,
-                        (const int*)s->run_state));
+                        (const int*)s->run_state, (const int32_t*)nullptr));
   }
   int ss_parts = 1;
   if (s->tc && s->mk_dirty) {   // layer table + merge slots (never inside a capture)
@@ -950,9 +964,11 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
                       (const int*)s->run_state, (const int32_t*)s->cell_pos, s->cell_mask,
                       io.out_status));
   if (head && head->nrows > 0) {
-    SP_CHECK(launch_pdl(gather_rows_kernel, dim3(head->nrows), dim3(128), 0, st,
-                        (const float*)x_out, d, (const int32_t*)s->hdr_rows, s->xg,
-                        (const int*)s->run_state));
+    const bool tc_head = s->tc && s->w_out_tc && head->nrows <= s->max_tokens;
+    if (!tc_head)
+      SP_CHECK(launch_pdl(gather_rows_kernel, dim3(head->nrows), dim3(128), 0, st,
+                          (const float*)x_out, d, (const int32_t*)s->hdr_rows, s->xg,
+                          (const int*)s->run_state));
     LmArgs m{};
     m.w = s->w_out; m.V = D.vocab; m.d = d; m.x = s->xg; m.n_rows = head->nrows;
     m.norm = 1; m.eps = D.norm_eps;
@@ -965,7 +981,28 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     m.chain_gate = head->chain_gate;
     m.hdr = s->hdr;
     m.swz = s->swz;
-    SP_CHECK(launch_lmhead(m, D.w_dtype, st));
+    if (tc_head) {
+      // tensor-core head: the flagged rows gathered as bf16 x*g_final (+ their
+      // statistic) into the stage's xb / ss, one tcgen05 GEMM over the tiled
+      // head with the fused greedy epilogue -- flat in rows (<= 16 per pass)
+      SP_CHECK(launch_pdl(prep_kernel, dim3(head->nrows), dim3(256), 0, st, (const float*)x_out,
+                          d, m.gain, s->xb, s->ss, (const int*)s->run_state,
+                          (const int32_t*)s->hdr_rows));
+      TcArgs h{};
+      h.w = s->w_out_tc; h.n_rows = D.vocab; h.k = d; h.m = head->nrows;
+      h.epi = SP_EPI_LMHEAD; h.norm = 1; h.norm_eps = D.norm_eps;
+      h.out = head->logits; h.ldo = D.vocab;
+      h.ss_in = s->ss; h.ss_nparts = 1; h.ss_ld = s->max_tokens;
+      h.scratch = s->tc_scratch; h.tickets = s->tc_tickets; h.ksplit = 1;
+      h.max_ctas = s->tc_ctas; h.err = s->err; h.run_state = s->run_state;
+      h.lm_out = head->out; h.lm_part = s->lm_scratch; h.lm_ticket = s->lm_ticket;
+      h.lm_err_out = head->err_out; h.lm_status_out = head->status_out;
+      h.lm_tip = m.tip; h.lm_gate = m.gate; h.lm_chain_gate = head->chain_gate;
+      h.lm_hdr = s->hdr;
+      SP_CHECK(launch_tc_gemm(s->m_xb, h, st));
+    } else {
+      SP_CHECK(launch_lmhead(m, D.w_dtype, st));
+    }
   }
   return SP_OK;
 }

@@ -30,6 +30,29 @@ namespace sp {
 constexpr int TC_THREADS = 128;
 constexpr int TC_STAGES = 4;
 
+// greedy-head order: (a before b) iff a.v > b.v or (a.v == b.v and a.i < b.i)
+__device__ __forceinline__ bool tc_better(float va, int ia, float vb, int ib) {
+  return va > vb || (va == vb && ia < ib);
+}
+struct TcTop2 { float v1; int i1; float v2; int i2; };
+__device__ __forceinline__ void tc_push(TcTop2& t, float v, int i) {
+  if (tc_better(v, i, t.v1, t.i1)) { t.v2 = t.v1; t.i2 = t.i1; t.v1 = v; t.i1 = i; }
+  else if (tc_better(v, i, t.v2, t.i2)) { t.v2 = v; t.i2 = i; }
+}
+__device__ __forceinline__ void tc_top2_butterfly(TcTop2& t, float& mx, int& nan) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float v1 = __shfl_xor_sync(0xffffffffu, t.v1, o);
+    const int i1 = __shfl_xor_sync(0xffffffffu, t.i1, o);
+    const float v2 = __shfl_xor_sync(0xffffffffu, t.v2, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, t.i2, o);
+    tc_push(t, v1, i1);
+    tc_push(t, v2, i2);
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+  }
+}
+
 template <int ST>
 struct TcSmemTailT {
   uint64_t full[ST];
@@ -119,6 +142,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
   pdl_trigger();
   const int npre_done = tail->npre;
   if (run_skipped(a.run_state)) {        // consistent for the whole grid (no one waits)
+    if (EPI == SP_EPI_LMHEAD && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+      if (a.lm_gate) *a.lm_gate = 0;     // (lmhead_kernel's skipped-run contract)
+      if (a.lm_err_out) *a.lm_err_out = a.err ? *a.err : 0;
+      if (a.lm_status_out) *a.lm_status_out = SP_STATUS_PLACEHOLDER;
+    }
     if (threadIdx.x == 0) {              // drain the weight prefetch
       for (int i = 0; i < npre_done; ++i) {
         mbar_arrive(&tail->full[i]);
@@ -393,6 +421,96 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
                                 __fadd_rn(tail->ssw[2][c], tail->ssw[3][c]));
       a.ss_out[(size_t)tile * a.ss_ld + a.tok0 + c] = s;
     }
+  } else if (EPI == SP_EPI_LMHEAD) {
+    // greedy head (model.py:424-457): per token the tile's top-2 (value
+    // desc, id asc), max and sum of exp over its 128 vocabulary rows, then
+    // the last tile CTA merges the tiles in tile order (fixed: the record
+    // does not depend on scheduling or on how many tokens share the launch)
+    float* tv = reinterpret_cast<float*>(smem);           // [NT][128]; stages are idle
+#pragma unroll
+    for (int c = 0; c < NT; ++c) {
+      if (c >= mv) break;
+      float y = acc[c];
+      if (NORM) y = __fmul_rn(y, tail->inv_rms[c]);
+      tv[c * TC_BM + row] = y;
+      if (a.out) reinterpret_cast<float*>(a.out)[(size_t)(a.tok0 + c) * a.ldo + R] = y;
+    }
+    __syncthreads();
+    const int ntiles = gridDim.x;
+    LmPartial* part = reinterpret_cast<LmPartial*>(a.lm_part);
+    for (int c = warp; c < mv; c += TC_THREADS / 32) {
+      float v[4];
+      TcTop2 t{-INFINITY, 0x7fffffff, -INFINITY, 0x7fffffff};
+      float mx = -INFINITY;
+      int nan = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[i] = tv[c * TC_BM + lane + 32 * i];
+        if (isnan(v[i])) nan = 1;
+        else { tc_push(t, v[i], tile * TC_BM + lane + 32 * i); mx = fmaxf(mx, v[i]); }
+      }
+      tc_top2_butterfly(t, mx, nan);
+      float se = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (!isnan(v[i]) && mx != -INFINITY) se = __fadd_rn(se, __expf(v[i] - mx));
+      se = warp_sum(se);
+      if (lane == 0)
+        part[(size_t)(a.tok0 + c) * ntiles + tile] = LmPartial{t.v1, t.i1, t.v2, t.i2, mx, se, nan, 0};
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) tail->last = atomicAdd(a.lm_ticket, 1) == ntiles - 1;
+    __syncthreads();
+    if (!tail->last) return;
+    __threadfence();
+    for (int c = warp; c < mv; c += TC_THREADS / 32) {   // one warp per token
+      const LmPartial* P = part + (size_t)(a.tok0 + c) * ntiles;
+      TcTop2 t{-INFINITY, 0x7fffffff, -INFINITY, 0x7fffffff};
+      float mx = -INFINITY;
+      int nan = 0;
+      for (int q = lane; q < ntiles; q += 32) {
+        const float4 lo = __ldcg(reinterpret_cast<const float4*>(P + q));
+        const float4 hi = __ldcg(reinterpret_cast<const float4*>(P + q) + 1);
+        tc_push(t, lo.x, __float_as_int(lo.y));
+        tc_push(t, lo.z, __float_as_int(lo.w));
+        mx = fmaxf(mx, hi.x);
+        nan |= __float_as_int(hi.z);
+      }
+      tc_top2_butterfly(t, mx, nan);
+      float se = 0.f;
+      for (int q = lane; q < ntiles; q += 32) {
+        const float2 ms = __ldcg(reinterpret_cast<const float2*>(P + q) + 2);
+        if (ms.x != -INFINITY) se = __fadd_rn(se, __fmul_rn(ms.y, __expf(ms.x - mx)));
+      }
+      se = warp_sum(se);
+      if (lane == 0) {
+        sp_row_result r;
+        r.argmax = t.i1;
+        r.second = t.i2;
+        r.conf = 1.0f / se;        // exp(max - max) / sum
+        r.max_logit = t.v1;
+        a.lm_out[a.tok0 + c] = r;
+        if (nan) set_error(a.err, SP_DEV_NAN_LOGITS);
+        if (a.lm_tip && a.tok0 + c == a.m - 1) {
+          a.lm_tip[0] = r.argmax;
+          a.lm_tip[1] = __float_as_int(r.conf);
+          a.lm_tip[2] = 1;
+          if (a.lm_gate && a.lm_chain_gate) {
+            const int g = *a.lm_gate;
+            const float cut = a.lm_hdr ? reinterpret_cast<const RunHdr*>(a.lm_hdr)->cutoff
+                                       : a.lm_cutoff;
+            *a.lm_gate = (g != 0 && r.conf >= cut) ? 1 : 0;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *a.lm_ticket = 0;
+      if (a.lm_err_out) *a.lm_err_out = a.err ? *a.err : 0;
+      if (a.lm_status_out) *a.lm_status_out = SP_STATUS_VALID;
+    }
   } else {  // SP_EPI_STORE
 #pragma unroll
     for (int c = 0; c < mv; ++c) {
@@ -497,6 +615,9 @@ static cudaError_t launch_epi(const CUtensorMap& x, const TcArgs& a, int ksplit,
                     : launch_nt<NT, SP_EPI_SWIGLU, false, ST>(x, a, ksplit, st);
     case SP_EPI_RESID:
       return launch_nt<NT, SP_EPI_RESID, false, ST>(x, a, ksplit, st);
+    case SP_EPI_LMHEAD:
+      return a.norm ? launch_nt<NT, SP_EPI_LMHEAD, true, ST>(x, a, ksplit, st)
+                    : launch_nt<NT, SP_EPI_LMHEAD, false, ST>(x, a, ksplit, st);
     case SP_EPI_STORE:
       return a.norm ? launch_nt<NT, SP_EPI_STORE, true, ST>(x, a, ksplit, st)
                     : launch_nt<NT, SP_EPI_STORE, false, ST>(x, a, ksplit, st);

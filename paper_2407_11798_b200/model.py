@@ -226,6 +226,7 @@ class DeviceModel:
         self.embedding = None     # [V, d]
         self.pos_table = None     # [max_context, d] fp32 (ref)
         self.w_out = None         # [V, d]
+        self.w_out_tc = None      # the same, tensor-core tiled (llama, V % 128 == 0)
         self.final_norm = None    # [d] fp32 (llama)
         self.layers = {}          # layer -> dict of device tensors
         self.host = None
@@ -463,6 +464,10 @@ def build_model(config: ModelConfig, device=None, layer_range=None,
         m.w_out = draw(1, (config.vocab_size, d), 1 / math.sqrt(d))
         if m.swz:
             m.w_out = swz8_weight(m.w_out)
+        elif m.tiled and config.vocab_size % 128 == 0 and d % 64 == 0:
+            # the tensor-core head's copy (stage steps); the row-major one
+            # serves the CUDA-core head entry points and the host views
+            m.w_out_tc = tile_weight(m.w_out)
         m.final_norm = ones.clone()
     return m
 

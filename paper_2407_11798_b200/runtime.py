@@ -9,6 +9,7 @@ and the API-mirror conveniences (``eval_batch``, ``decode_step``) wait.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional, Sequence
 
 import numpy as np
@@ -65,6 +66,10 @@ class Stage:
                                               _ptr(L["mlp_norm"])))
         if hi == cfg.n_layers and model.w_out is not None:
             check(self.lib.sp_stage_set_head(h, _ptr(model.w_out), _ptr(model.final_norm)))
+            if getattr(model, "w_out_tc", None) is not None and \
+                    os.environ.get("SP_LMHEAD_CUDA_CORES") != "1":
+                check(self.lib.sp_stage_set_head_tiled(h, _ptr(model.w_out_tc)),
+                      "sp_stage_set_head_tiled")
         if cancel_table is not None:
             self.set_cancel_table(cancel_table, cancel_size)
         d = cfg.embed_dim

@@ -23,15 +23,23 @@ for c0 in range(0, ctx, 128):
     chunk = pre[c0:c0 + 128]
     pipe.launch(c0, 0, encode_tokens(chunk), 0, [len(chunk) - 1])
     pipe.wait()
+M = int(os.environ.get("M", "1"))   # tokens per run (a verification run when > 1)
 rid = 1000
-for rep in range(4):   # warm + capture the graph
-    pipe.launch(rid, 1, encode_tokens([BatchToken(7, ctx + rep, frozenset([0]), True)]), 0, [0])
+
+
+def run_batch(p0):
+    toks = [BatchToken(7 + i, p0 + i, frozenset([0]), True) for i in range(M)]
+    pipe.launch(rid, 1 if M == 1 else 2, encode_tokens(toks), 0, list(range(M)))
     pipe.wait()
+    pipe.remove(0, p0 + 1)       # keep one cell per run: contexts grow by one
+
+
+for rep in range(4):   # warm + capture the graph
+    run_batch(ctx + rep)
     rid += 1
 torch.cuda.synchronize()
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
-    pipe.launch(rid, 1, encode_tokens([BatchToken(7, ctx + 4, frozenset([0]), True)]), 0, [0])
-    pipe.wait()
+    run_batch(ctx + 4)
     torch.cuda.synchronize()
 prof.export_chrome_trace("/tmp/st.json")
 ev = [e for e in json.load(open("/tmp/st.json"))["traceEvents"] if e.get("cat") == "kernel"]
