@@ -425,6 +425,11 @@ class Head:
         one = pipe.n_stages == 1
         shared = bool(getattr(draft, "shared_gpu", True))
         self.adaptive = cfg.fold_frontier is None and not one
+        # a 1-stage pipeline with a draft GPU of its own speculates one run
+        # ahead only while chains break often (alpha < 0.75): measured N=2
+        # alpha 0.66 540 vs 497 tok/s sync, but alpha 0.9 662 vs 946 with
+        # the run ahead (its continuation runs crowd out folded runs)
+        self.adapt_cap = cfg.max_inflight is None and one and not shared
         self.fold_frontier = one if cfg.fold_frontier is None else bool(cfg.fold_frontier)
         self._fold_cap = (1 if shared else 2) if one else pipe.n_stages
         self.max_inflight = ((self._fold_cap if self.fold_frontier else 0)
@@ -953,6 +958,8 @@ class Head:
         self._cancel_stale()
         if self.adaptive:
             self._adapt_policy()
+        elif self.adapt_cap and self.examined >= 16:
+            self.max_inflight = 2 if self.matched / self.examined < 0.75 else 1
         if self.generated < self.cfg.gen_len and not self.terminal:
             if not self._frontier_carried():
                 if (self.fold_frontier and self.draft is not None
@@ -963,13 +970,21 @@ class Head:
 
     def _adapt_policy(self) -> None:
         """Fold the frontier (and cap in-flight runs at the stage count) while
-        a micro-batch of draft forwards costs less than one stage-time and
-        the running acceptance is >= 0.5; otherwise the reference policy."""
+        it pays: when a micro-batch of draft forwards costs less than one
+        stage-time and the running acceptance is >= 0.5, or whenever the
+        acceptance is >= 0.75 (long chains: one draft wait per mismatch buys
+        runs that carry several tokens).  Measured (profiles/r02_sweep_*):
+        7B, 3 stages: alpha 0.66 reference 577-590 vs folded 475 tok/s;
+        alpha 0.8 804 vs 913; alpha 0.9 1293 vs 1406; 70B alpha 0.66 (draft
+        far below a stage-time) 88 vs 100.  Otherwise the reference policy."""
         if self.est_draft_fwd is None or self.est_run is None:
             return
-        alpha = self.matched / self.examined if self.examined >= 16 else 0.5
+        if self.examined < 16:
+            return
+        alpha = self.matched / self.examined
         stage_time = self.est_run / self.pipe.n_stages
-        fold = alpha >= 0.5 and self.est_draft_fwd * self.cfg.microbatch < stage_time
+        cheap = self.est_draft_fwd * self.cfg.microbatch < stage_time
+        fold = (alpha >= 0.5 and cheap) or alpha >= 0.75
         self.fold_frontier = fold
         if self.cfg.max_inflight is None:
             self.max_inflight = self._fold_cap if fold else 0
