@@ -535,6 +535,7 @@ cudaError_t launch_attention(const AttnArgs& a0, int kv_dtype, int hd,
   if (diag == 2) return cudaSuccess;   // diagnostics: no attention launch at all
   a.diag_empty = diag == 1;
   if (attn_tc_ok(kv_dtype, hd, a.n)) return launch_attention_tc(a, hd, st);
+  if (attn_fd_ok(kv_dtype, hd, a.n, a.max_context)) return launch_attention_fd(a, hd, st);
   return kv_dtype == SP_DTYPE_BF16 ? attn_dispatch<__nv_bfloat16>(a, hd, st)
                                    : attn_dispatch<float>(a, hd, st);
 }

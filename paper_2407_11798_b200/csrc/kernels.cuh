@@ -59,6 +59,7 @@ struct AttnArgs {
   // that is a prefix of the reference's), or null
   const sp_token* toks;
   const RunHdr* hdr;
+  int max_context;   // the model's context cap (a per-stage constant: kernel choice)
 };
 
 struct LmPartial {
@@ -166,6 +167,9 @@ cudaError_t launch_plan(const int32_t* cell_pos, const uint32_t* cell_mask,
 cudaError_t launch_attention(const AttnArgs& a, int kv_dtype, int hd,
                              cudaStream_t st);
 int attn_splits(int max_len);
+// flash-decoding attention over bf16 caches, decode-sized runs (attention_fd.cu)
+bool attn_fd_ok(int kv_dtype, int hd, int n, int max_context);
+cudaError_t launch_attention_fd(const AttnArgs& a, int hd, cudaStream_t st);
 // tensor-core attention over bf16 caches (attention_tc.cu)
 bool attn_tc_ok(int kv_dtype, int hd, int n);
 cudaError_t launch_attention_tc(const AttnArgs& a, int hd, cudaStream_t st);

@@ -841,6 +841,7 @@ static int enqueue_run(sp_stage* s, int n, int layer_a, int layer_b, bool cont,
     a.fresh_row0_dev = row0_dev;   // the QKV epilogue writes rows row0 .. row0 + n
     a.toks = s->hdr_toks;
     a.hdr = (const RunHdr*)s->hdr;
+    a.max_context = D.max_context;
     if (s->tc) {
       // ---- tensor-core path (tcgen05, bf16 activations, fp32 accumulate) ----
       TcArgs t{};

@@ -11,6 +11,7 @@ import torch
 
 import paper_2407_11798_b200 as sp
 from paper_2407_11798_b200.model import BatchToken, encode_tokens
+from paper_2407_11798_b200 import _lib
 from paper_2407_11798_b200.pipeline import LocalPipeline
 
 ctx_arg = int(sys.argv[1]) if len(sys.argv) > 1 else 384
@@ -29,7 +30,9 @@ rid = 1000
 
 def run_batch(p0):
     toks = [BatchToken(7 + i, p0 + i, frozenset([0]), True) for i in range(M)]
-    pipe.launch(rid, 1 if M == 1 else 2, encode_tokens(toks), 0, list(range(M)))
+    # (coverage-checked, as every engine run is)
+    pipe.launch(rid, 1 if M == 1 else 2, encode_tokens(toks), _lib.SP_FWD_CHECK_COVERAGE,
+                list(range(M)))
     pipe.wait()
     pipe.remove(0, p0 + 1)       # keep one cell per run: contexts grow by one
 
