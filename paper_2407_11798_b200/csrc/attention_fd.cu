@@ -25,7 +25,10 @@ namespace sp {
 
 constexpr int FD_C = 64;          // plan entries per chunk
 constexpr int FD_THREADS = 128;
-constexpr int FD_QB = 4;          // queries per register batch
+#ifndef SP_FD_QB
+#define SP_FD_QB 4
+#endif
+constexpr int FD_QB = SP_FD_QB;   // queries per register batch
 
 __device__ __forceinline__ uint32_t fd_s(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
