@@ -127,7 +127,8 @@ class _DraftBase:
         self.forwards += (1 if feed else 0) + steps
         with torch.cuda.stream(self.stream):
             self.rows_host.copy_(self.rows, non_blocking=True)
-            self.res_host.copy_(self.res, non_blocking=True)
+            if self._blocks:      # (only a batched feed forward left a result block)
+                self.res_host.copy_(self.res, non_blocking=True)
         self.event.record(self.stream)
 
     def _chain(self, feed: Sequence[int], steps: int, cutoff: float) -> None:
