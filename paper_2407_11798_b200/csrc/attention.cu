@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
     for (int ss = 0; ss < ns; ++ss) {
       const float* b = src + ss * (HD + 2);
       const float m0 = a.merge_smem ? b[0] : __ldcg(b), l0 = a.merge_smem ? b[1] : __ldcg(b + 1);
-      L += l0 * __expf(m0 - M);
+      L = __fmaf_rn(l0, __expf(m0 - M), L);
     }
     for (int d = tid; d < HD; d += ATT_THREADS) {
       float o = 0.f;
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_kernel(const AttnArgs a) {
         const float* b = src + ss * (HD + 2);
         const float m0 = a.merge_smem ? b[0] : __ldcg(b);
         const float ov = a.merge_smem ? b[2 + d] : __ldcg(b + 2 + d);
-        o += ov * __expf(m0 - M);
+        o = __fmaf_rn(ov, __expf(m0 - M), o);
       }
       store(d, o / L);
     }
