@@ -1211,12 +1211,16 @@ class Engine:
                   "pipeline-iterative": head.run_iterative,
                   "sync-speculative": head.run_sync_speculative,
                   "async-speculative": head.run_async_speculative}[cfg.mode]
+        comp0 = getattr(self.pipe, "compactions", 0)
         runner()
         wall = time.perf_counter() - wall0
         self.last_head_policy = {"fold_frontier": head.fold_frontier,
                                  "max_inflight": head.max_inflight,
                                  "adaptive": head.adaptive, "folded_runs": head.folded_runs,
-                                 "sibling_hits": head.sibling_hits}
+                                 "sibling_hits": head.sibling_hits,
+                                 # cell-pool compactions in this run (each drains
+                                 # the stages' streams once: dist.py R_COMPACT)
+                                 "compactions": getattr(self.pipe, "compactions", 0) - comp0}
         metrics = head.build_metrics(wall)
         sent = dict(head.msgs)
         node_logs = dict(head.stage_logs)
