@@ -566,16 +566,30 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
           const int grp = tid / LPR, li = tid % LPR;
           const int kh = hh / (a.H / a.KH);
           const int len = rowA + 1;
-          float qv[8];
-          {
-            const float* qp = a.q + hh * HD + li * 8;
-            const float4 q0 = __ldcg(reinterpret_cast<const float4*>(qp));
-            const float4 q1 = __ldcg(reinterpret_cast<const float4*>(qp + 4));
-            qv[0] = q0.x * att_scale; qv[1] = q0.y * att_scale;
-            qv[2] = q0.z * att_scale; qv[3] = q0.w * att_scale;
-            qv[4] = q1.x * att_scale; qv[5] = q1.y * att_scale;
-            qv[6] = q1.z * att_scale; qv[7] = q1.w * att_scale;
+          // this member's W_o rows do not depend on the attention: their
+          // loads go out first and land while it runs (one HBM round trip
+          // off the phase)
+          const int r0 = (int)(((long)d * jm) / GS), r1 = (int)(((long)d * (jm + 1)) / GS);
+          constexpr int LR = HD / 8, RW = 32 / LR;
+          constexpr int WB = 4;
+          const int lr = lane % LR, rw = lane / LR;
+          const bool wone = r1 - r0 <= DR_WARPS * RW * WB;   // one batch covers the slice
+          uint4 wpre[WB];
+          if (wone) {
+#pragma unroll
+            for (int b = 0; b < WB; ++b) {
+              const int r = r0 + warp * RW + b * DR_WARPS * RW + rw;
+              const int un = (hh * HD) / 8 + lr;
+              wpre[b] = r < r1 ? ld_stream16(Lw.o + (size_t)r * qd + (size_t)(un ^ (r & 7)) * 8)
+                               : make_uint4(0, 0, 0, 0);
+            }
           }
+          // q is scaled only after the first chunk's K/V loads are out (the
+          // loads share one round trip)
+          const float* qp = a.q + hh * HD + li * 8;
+          const float4 q0 = __ldcg(reinterpret_cast<const float4*>(qp));
+          const float4 q1 = __ldcg(reinterpret_cast<const float4*>(qp + 4));
+          float qv[8];
           // per row-group online softmax over rows grp, grp+RPP, ... (fixed order)
           float mx = -INFINITY, ls = 0.f, acc[8];
 #pragma unroll
@@ -589,6 +603,10 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
               kr[p] = r < len ? ldcg16(Kc + off) : make_uint4(0, 0, 0, 0);
               vr[p] = r < len ? ldcg16(Vc + off) : make_uint4(0, 0, 0, 0);
             }
+            qv[0] = q0.x * att_scale; qv[1] = q0.y * att_scale;
+            qv[2] = q0.z * att_scale; qv[3] = q0.w * att_scale;
+            qv[4] = q1.x * att_scale; qv[5] = q1.y * att_scale;
+            qv[6] = q1.z * att_scale; qv[7] = q1.w * att_scale;
 #pragma unroll
             for (int p = 0; p < PASSES; ++p) {
               const int r = c0 + p * RPP + grp;
@@ -635,24 +653,22 @@ __global__ void __launch_bounds__(DR_THREADS, 1) draft_chain_kernel(const DraftA
           }
           __syncthreads();
           // this member's rows of the head's O columns (SWZ8 units)
-          const int r0 = (int)(((long)d * jm) / GS), r1 = (int)(((long)d * (jm + 1)) / GS);
-          constexpr int LR = HD / 8, RW = 32 / LR;
-          const int lr = lane % LR, rw = lane / LR;
           float av[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) av[j] = attn_s[lr * 8 + j];
           float* op = a.opart + (size_t)hh * d;
-          for (int rb = r0 + warp * RW; rb < r1; rb += DR_WARPS * RW * 4) {
-            uint4 wv[4];
+          for (int rb = r0 + warp * RW; rb < r1; rb += DR_WARPS * RW * WB) {
+            uint4 wv[WB];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 0; b < WB; ++b) {
               const int r = rb + b * DR_WARPS * RW + rw;
               const int un = (hh * HD) / 8 + lr;
-              wv[b] = r < r1 ? ld_stream16(Lw.o + (size_t)r * qd + (size_t)(un ^ (r & 7)) * 8)
-                             : make_uint4(0, 0, 0, 0);
+              wv[b] = wone ? wpre[b]
+                      : r < r1 ? ld_stream16(Lw.o + (size_t)r * qd + (size_t)(un ^ (r & 7)) * 8)
+                               : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 0; b < WB; ++b) {
               float wf[8];
               bf16x8_to_f32(wv[b], wf);
               float t = 0.f;

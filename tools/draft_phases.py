@@ -18,6 +18,9 @@ shape = sys.argv[1] if len(sys.argv) > 1 else "llama-160m"
 cfg = sp.llama_config(shape)
 dm = sp.build_model(cfg, dev, tiled=False)
 srv = TableDraftServer(dm, list(range(2000)), list(range(2000)), 0.66, 1)
+if os.environ.get("KIND", "grid") == "grid":   # the exclusive (whole-GPU) kernel, draft.cu
+    srv.shared_gpu = True
+    srv.set_exclusive(True)
 srv.request(0, list(range(128)), 0, 1.0); srv.reply()
 for _ in range(5):
     srv.request(len(srv), [7], 4, 0.0); srv.reply()
