@@ -647,7 +647,9 @@ int tc_ksplit(int n_rows, int k, int target_ctas) {
   // the split CTAs of a tile merge as one cluster: at most 8 (portable size),
   // a power of two (odd clusters schedule badly: measured QKV 18.5 us at 2,
   // 26.5 at 3; O 11.0 at 4; down 18.7 at 8 on the 7B shapes)
-  int ks = max(1, min(min(target_ctas / tiles, nchunk / 16), 8));
+  static const int min_chunks =
+      getenv("SP_TC_MIN_CHUNKS") ? max(1, atoi(getenv("SP_TC_MIN_CHUNKS"))) : 16;   // experiments
+  int ks = max(1, min(min(target_ctas / tiles, nchunk / min_chunks), 8));
   while (ks & (ks - 1)) ks &= ks - 1;
   return ks;
 }
