@@ -407,9 +407,19 @@ def init(max_tokens: int = 256):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # SP_DIST_GPUS=G (tests only): more ranks than GPUs, rank r on GPU r % G.
+    # The world group is then gloo (NCCL refuses two ranks of one GPU in a
+    # communicator); the activation pairs (r, r + 1) sit on different GPUs
+    # and stay NCCL.  Timings of such a run mean nothing.
+    oversub = int(os.environ.get("SP_DIST_GPUS", "0"))
+    if oversub:
+        local = local % oversub
     torch.cuda.set_device(local)
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     gloo = dist.new_group(backend="gloo")
     # one NCCL communicator per adjacent pair: a rank's receive (from i-1)
     # and send (to i+1) then run on different streams instead of being

@@ -45,3 +45,29 @@ def test_multi_gpu_streams_match(tmp_path):
         for mode in ("async-speculative", "sync-speculative", "pipeline-iterative",
                      "async-speculative:tree", "sync-speculative:tree"):
             assert got[mode] == want, (case, mode)
+
+
+def test_world8_streams_match_oversubscribed(tmp_path):
+    """The 8-rank pipeline (7 stages + dedicated head/draft rank, or 8
+    shared stages) on the GPUs a box has: ranks r on GPU r % G (SP_DIST_GPUS,
+    world group on gloo, activation pairs on NCCL across two GPUs).  Streams
+    must equal the oracle / 1-GPU references exactly as at N <= 4."""
+    import torch
+    g = min(4, torch.cuda.device_count())
+    if g < 2:
+        pytest.skip("needs >= 2 GPUs")
+    out = tmp_path / "streams8.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=8", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "dist_parity_main.py"),
+           str(out)]
+    env = dict(os.environ, SP_DIST_GPUS=str(g))
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    d = json.loads(out.read_text())
+    assert d["world"] == 8
+    for case, got in d["results"].items():
+        want = d["refs"][case.split("/")[0]]
+        for mode in ("async-speculative", "sync-speculative", "pipeline-iterative",
+                     "async-speculative:tree", "sync-speculative:tree"):
+            assert got[mode] == want, (case, mode)
