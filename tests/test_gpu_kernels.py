@@ -222,3 +222,30 @@ def test_tc_gemm_resid_swiglu(env):
     z = Xq @ Wq.T
     sw = z[:, 0::2] / (1 + np.exp(-z[:, 0::2])) * z[:, 1::2]
     assert np.abs(hb.float().cpu().numpy() - sw).max() < 2e-2
+
+
+
+def test_attention_grid_and_merge_path_bitwise(tmp_path):
+    """The decode attention's bits do not depend on its grid or merge path
+    (attention.cu attn_kernel): one split per CTA equals CTAs looping over
+    several splits, and merging the split partials from shared memory
+    equals merging them from L2 -- on chains, tree siblings and arbitrary
+    per-query plans, head dims 64 / 128, GQA; every output is also checked
+    against fp32 (model.py:394-415)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for name, extra in (("base", {}), ("loops", {"SP_ATT_CTAS_PER_SM": "1"}),
+                        ("l2merge", {"SP_ATT_MERGE_SMEM_KB": "0"})):
+        path = str(tmp_path / f"{name}.npz")
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, os.path.join(root, "tests", "attn_variant_main.py"),
+                            path], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+        outs[name] = np.load(path)
+    base = outs["base"]
+    for name in ("loops", "l2merge"):
+        for key in base.files:
+            assert np.array_equal(base[key], outs[name][key]), (name, key)
