@@ -623,6 +623,13 @@ def main():
                          "(the reference's nodes = stages + draft node); auto = on "
                          "(measured: the dedicated layout wins at N=2 and N=4)")
     args = ap.parse_args()
+    if (args.depth is None and args.microbatch is None and not args.reference_policy
+            and args.tree_width in (None, 1)):
+        # speculation depth (proposals per run) by layout, for async and the
+        # sync baseline alike (profiles/r02_sweep_depth.txt, alpha 0.66):
+        # N=1 3 > 4, N=2 4 > 3, N=4 2-3 > 4.  The engine's own default stays
+        # the reference's microbatch 4.
+        args.depth = 4 if args.gpus == 2 else 3
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None and int(os.environ.get("RANK", "0")) == 0:
         print(json.dumps(line), flush=True)
