@@ -407,7 +407,7 @@ def measure(eng, args, n_gpus: int, pipe=None) -> dict:
     itl = statistics.mean(r.metrics.itl for r in res)
     # baselines on the same kernels and pipeline: sync-speculative (the >=2x
     # target's denominator) and plain pipeline-iterative decoding
-    nb = min(2, args.steps)
+    nb = args.steps     # the same prompts as the timed async steps
     sync = [eng.run(prompt_seed=seeds[args.warmup + i], mode="sync-speculative")
             for i in range(nb)]
     itr = [eng.run(prompt_seed=seeds[args.warmup + i], mode="pipeline-iterative")
@@ -627,9 +627,9 @@ def main():
             and args.tree_width in (None, 1)):
         # speculation depth (proposals per run) by layout, for async and the
         # sync baseline alike (profiles/r02_sweep_depth.txt, alpha 0.66):
-        # N=1 3 > 4, N=2 4 > 3, N=4 2-3 > 4.  The engine's own default stays
+        # N=1 3 > 4, N=2 4 > 3, N=4 2 > 3 > 4.  The engine's own default stays
         # the reference's microbatch 4.
-        args.depth = 4 if args.gpus == 2 else 3
+        args.depth = 3 if args.gpus == 1 else 4 if args.gpus == 2 else 2
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None and int(os.environ.get("RANK", "0")) == 0:
         print(json.dumps(line), flush=True)
