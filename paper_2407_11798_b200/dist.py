@@ -125,7 +125,7 @@ class ControlPlane:
             lag = min(int(self.hdr[8 + r]) for r in range(1, self.n_ranks))
             if idx - lag < RING:
                 break
-            time.sleep(0)
+            os.sched_yield()
         if len(payload) + 8 > SLOT:
             raise ValueError("control record too large")
         rec = self.ring[idx % RING]
@@ -137,7 +137,7 @@ class ControlPlane:
     def read(self, rank: int):
         idx = self.cursor
         while int(self.hdr[1]) <= idx:
-            time.sleep(0)
+            os.sched_yield()
         rec = self.ring[idx % RING]
         rtype, n = struct.unpack("<ii", rec[:8].tobytes())
         payload = rec[8:8 + n].tobytes()
@@ -384,7 +384,7 @@ class DistPipeline:
         if not self.fifo:
             raise RuntimeError("wait with an empty FIFO")
         while not self.ready():
-            time.sleep(0)
+            os.sched_yield()
         return self._collect()
 
     def in_flight(self) -> int:

@@ -18,6 +18,7 @@ own stream (``drafting.py``).  All times are host wall-clock seconds.
 from __future__ import annotations
 
 import hashlib
+import os
 import time
 from collections import deque
 from dataclasses import dataclass, field, fields, replace
@@ -734,10 +735,12 @@ class Head:
         """recv_any([LOGITS, DRAFT_REPLY]) without consuming (the loop does)."""
         if self.pipe.in_flight() == 0 and not self.draft_busy:
             raise EngineError("deadlock: nothing in flight and nothing to launch")
+        # (a yield, not time.sleep(0): the kernel's default 50 us timer slack
+        # made every poll a ~55 us sleep -- twice per speculation cycle at N=1)
         while True:
             if self.pipe.ready() or (self.draft_busy and self.draft.ready()):
                 return
-            time.sleep(0)
+            os.sched_yield()
 
     # -- async internals (engine.py:1002-1182) -----------------------------------------
     def _want_speculation(self) -> bool:
