@@ -34,6 +34,12 @@ from .model import PREFILL, KIND_CODE, BatchToken, encode_tokens
 from .runtime import RES_DTYPE, Stage
 
 
+def _check_rc(rc: int) -> None:
+    if rc:
+        from . import _lib
+        _lib.check(rc, "sp_copy_async")
+
+
 class _DraftBase:
     def __init__(self, draft_model, stream=None, capacity: Optional[int] = None,
                  max_tokens: int = 256, stage: Optional[Stage] = None):
@@ -125,10 +131,14 @@ class _DraftBase:
         self.stage.decode_chain(feed, pos0, steps, cutoff, self.rows.data_ptr(),
                                 self.rows[65].data_ptr(), step_tokens)
         self.forwards += (1 if feed else 0) + steps
-        with torch.cuda.stream(self.stream):
-            self.rows_host.copy_(self.rows, non_blocking=True)
-            if self._blocks:      # (only a batched feed forward left a result block)
-                self.res_host.copy_(self.res, non_blocking=True)
+        # result rows to pinned host memory, stream-ordered (a direct async
+        # copy: no torch stream context on the request's critical path)
+        lib, st = self.stage.lib, self._raw_stream()
+        _check_rc(lib.sp_copy_async(self.rows_host.data_ptr(), self.rows.data_ptr(),
+                                    self.rows.numel() * 4, st))
+        if self._blocks:      # (only a batched feed forward left a result block)
+            _check_rc(lib.sp_copy_async(self.res_host.data_ptr(), self.res.data_ptr(),
+                                        self.res.numel() * 4, st))
         self.event.record(self.stream)
 
     def _chain(self, feed: Sequence[int], steps: int, cutoff: float) -> None:
@@ -158,10 +168,16 @@ class _DraftBase:
         self._blocks.append(block)
 
     def _finish_enqueue(self, nrows: int) -> None:
-        import torch
-        with torch.cuda.stream(self.stream):
-            self.res_host.copy_(self.res, non_blocking=True)
+        _check_rc(self.stage.lib.sp_copy_async(self.res_host.data_ptr(), self.res.data_ptr(),
+                                               self.res.numel() * 4, self._raw_stream()))
         self.event.record(self.stream)
+
+    def _raw_stream(self):
+        import ctypes
+        h = getattr(self, "_stream_handle", None)
+        if h is None:
+            h = self._stream_handle = ctypes.c_void_p(self.stream.cuda_stream)
+        return h
 
     def _check_err(self) -> None:
         blocks, self._blocks = self._blocks, []
