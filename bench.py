@@ -625,11 +625,14 @@ def main():
     args = ap.parse_args()
     if (args.depth is None and args.microbatch is None and not args.reference_policy
             and args.tree_width in (None, 1)):
-        # speculation depth (proposals per run) by layout, for async and the
-        # sync baseline alike (profiles/r02_sweep_depth.txt, alpha 0.66):
-        # N=1 3 > 4, N=2 4 > 3, N=4 2 > 3 > 4.  The engine's own default stays
-        # the reference's microbatch 4.
-        args.depth = 3 if args.gpus == 1 else 4 if args.gpus == 2 else 2
+        # speculation depth (proposals per run) by layout and acceptance, for
+        # async and the sync baseline alike (profiles/r02_sweep_depth.txt):
+        # alpha 0.66: N=1 3 > 4, N=2 4 > 3, N=4 2 > 3 > 4; alpha 0.9: 4 at
+        # every N.  The engine's own default stays the reference's microbatch 4.
+        if args.alpha >= 0.8:
+            args.depth = 4
+        else:
+            args.depth = 3 if args.gpus == 1 else 4 if args.gpus == 2 else 2
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
     if line is not None and int(os.environ.get("RANK", "0")) == 0:
         print(json.dumps(line), flush=True)
