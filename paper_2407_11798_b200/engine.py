@@ -763,12 +763,24 @@ class Head:
 
     @staticmethod
     def _common_prefix(a: Sequence[int], b: Sequence[int]) -> int:
-        n = 0
-        for x, y in zip(a, b):
-            if x != y:
-                break
-            n += 1
-        return n
+        """Length of the common prefix (list slices compare in C: the head
+        runs this per draft request over the whole context)."""
+        if not (isinstance(a, list) and isinstance(b, list)):
+            a, b = list(a), list(b)
+        n = min(len(a), len(b))
+        if a[:n] == b[:n]:
+            return n
+        lo, hi = 0, n          # a[:lo] == b[:lo], a[:hi] != b[:hi]
+        while hi - lo > 16:
+            mid = (lo + hi) // 2
+            if a[lo:mid] == b[lo:mid]:
+                lo = mid
+            else:
+                hi = mid
+        for i in range(lo, hi):
+            if a[i] != b[i]:
+                return i
+        return hi
 
     def _backoff(self, cp: int, ctx: List[int]) -> Tuple[int, List[int]]:
         """F4(b): a context that is a strict prefix of the draft's state would
