@@ -674,10 +674,13 @@ cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st) 
   const int tiles = a.n_rows / TC_BM, nchunk = a.k / TC_BK;
   int ksplit;
   bool deep = false;
+  // The split is a function of the GEMM shape only -- the same for the
+  // 16-token and the 128-token tiles -- so a token's K-sum order (and bits)
+  // does not depend on how many tokens share its run.
   // deep when the tile count leaves room to split at least 2-way within one
   // CTA per SM (measured on the 7B shapes: O 10.9 -> 10.4 us, down 18.7 ->
   // 17.4; QKV (96 tiles) stays faster at 2 shallow CTAs per SM)
-  if (nt == 16 && getenv("SP_TC_SHALLOW") == nullptr &&
+  if (getenv("SP_TC_SHALLOW") == nullptr &&
       (a.ksplit > 0 ? tiles * a.ksplit <= sms : 2 * tiles <= sms)) {
     // one CTA per SM with a deep ring: split so the grid still fits one wave
     ksplit = a.ksplit > 0 ? a.ksplit
@@ -685,7 +688,7 @@ cudaError_t launch_tc_gemm(const CUtensorMap* xmaps, TcArgs a, cudaStream_t st) 
     static const int ks_cap = getenv("SP_TC_DEEP_KS_MAX") ? atoi(getenv("SP_TC_DEEP_KS_MAX")) : 8;
     if (a.ksplit <= 0 && ksplit > ks_cap) ksplit = ks_cap;
     while (ksplit & (ksplit - 1)) ksplit &= ksplit - 1;
-    deep = true;
+    deep = nt == 16;
   } else {
     ksplit = a.ksplit > 0 ? a.ksplit : tc_ksplit(a.n_rows, a.k, budget);
   }

@@ -225,6 +225,20 @@ def test_tc_gemm_resid_swiglu(env):
 
 
 
+@pytest.mark.parametrize("shape", [(4096, 4096), (4096, 11008), (12288, 4096)])
+def test_tc_gemm_tile_size_invariance(env, shape):
+    """A token's GEMM result is the same whether its run takes the 16-token
+    or the 128-token tile path (runs of <= 16 vs 17+ tokens): the split-K
+    partition is a function of the shape only (7B O / down / QKV shapes)."""
+    n, k = shape
+    r = np.random.default_rng(n + k)
+    W = r.standard_normal((n, k)) / np.sqrt(k)
+    X = r.standard_normal((20, k))
+    big, _, _, _ = _tc(env, W, X)                 # m = 20: the 128-token tile
+    small, _, _, _ = _tc(env, W, X[:4])           # m = 4: the 16-token tile
+    assert np.array_equal(big.cpu().numpy()[:4], small.cpu().numpy())
+
+
 def test_attention_grid_and_merge_path_bitwise(tmp_path):
     """The decode attention's bits do not depend on its grid or merge path
     (attention.cu attn_kernel): one split per CTA equals CTAs looping over
