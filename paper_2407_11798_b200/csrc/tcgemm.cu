@@ -28,6 +28,9 @@
 namespace sp {
 
 constexpr int TC_THREADS = 128;
+// 128-token tiles run their epilogue on 8 warps: two per TMEM lane quarter,
+// each over half the token columns (the per-element arithmetic is unchanged)
+__host__ __device__ constexpr int tc_threads(int nt) { return nt > 16 ? 256 : TC_THREADS; }
 constexpr int TC_STAGES = 4;
 
 // greedy-head order: (a before b) iff a.v > b.v or (a.v == b.v and a.i < b.i)
@@ -74,7 +77,7 @@ struct TcSmemTailT {
 // lets the next GEMM's CTAs become resident -- and prefetch their weights
 // before the dependency wait -- while this one drains
 template <int NT, int EPI, bool NORM, int ST>
-__global__ void __launch_bounds__(TC_THREADS)
+__global__ void __launch_bounds__(tc_threads(NT))
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const int push) {
   constexpr int XTILE = NT * TC_BK * 2;
   constexpr int STAGE = TC_WTILE + XTILE;
@@ -85,6 +88,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
   TcSmemTailT<ST>* tail = reinterpret_cast<TcSmemTailT<ST>*>(smem + ST * STAGE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NC = NT > 16 ? NT / 2 : NT;          // token columns per thread
+  const int q4 = warp & 3;                            // TMEM lane quarter (weight rows)
+  const int cb = NT > 16 ? (warp >> 2) * NC : 0;      // this thread's first column
   const int tile = blockIdx.x, split = blockIdx.y, nsplit = gridDim.y;
   const int nchunk = a.k / TC_BK;
   const int c0 = (int)((long)nchunk * split / nsplit);
@@ -163,14 +169,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
 
   // epilogue operands that do not depend on this GEMM, loaded while it
   // streams: per-token RMSNorm scales, the residual rows, the next gain
-  const int row = warp * 32 + lane;          // row within the tile
+  const int row = q4 * 32 + lane;            // row within the tile
   const int R = tile * TC_BM + row;          // global weight row
   const int mv = min(NT, a.m - a.tok0);
   // the CTA that runs the epilogue (ticket merge: whichever split arrives
   // last, so every split loads the epilogue operands)
   const bool head = push != 1 || split == 0;
   if (NORM && head && threadIdx.x >= 64) {   // warps 2-3: not the producer / MMA lanes
-    for (int c = threadIdx.x - 64; c < mv; c += 64) {
+    for (int c = threadIdx.x - 64; c < mv; c += tc_threads(NT) - 64) {
       float ssum = 0.f;
       for (int p = 0; p < a.ss_nparts; ++p)
         ssum = __fadd_rn(ssum, a.ss_in[(size_t)p * a.ss_ld + a.tok0 + c]);
@@ -238,14 +244,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
   // ---- epilogue: TMEM -> registers (thread = weight row, NT token columns)
   mbar_wait(&tail->done, 0);
   tc_fence_after();
-  float acc[NT];
+  float acc[NC];
   if (nloc > 0) {
 #pragma unroll
-    for (int c = 0; c < NT; c += 16)
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c, acc + c);
+    for (int c = 0; c < NC; c += 16)
+      tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + cb + c, acc + c);
   } else {
 #pragma unroll
-    for (int c = 0; c < NT; ++c) acc[c] = 0.f;
+    for (int c = 0; c < NC; ++c) acc[c] = 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -263,8 +269,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
     if (nsplit > 1) {
       float* part = a.scratch + ((size_t)tile * nsplit + split) * (NT * TC_BM);
 #pragma unroll
-      for (int c = 0; c < NT; ++c)
-        if (c < mv) part[c * TC_BM + row] = acc[c];
+      for (int c = 0; c < NC; ++c)
+        if (cb + c < mv) part[(cb + c) * TC_BM + row] = acc[c];
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) tail->last = atomicAdd(a.tickets + tile, 1) == nsplit - 1;
@@ -273,12 +279,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
       __threadfence();
       const float* p0 = a.scratch + (size_t)tile * nsplit * (NT * TC_BM);
 #pragma unroll
-      for (int c = 0; c < NT; ++c)
-        if (c < mv) acc[c] = __ldcg(p0 + c * TC_BM + row);
+      for (int c = 0; c < NC; ++c)
+        if (cb + c < mv) acc[c] = __ldcg(p0 + (cb + c) * TC_BM + row);
       for (int sp2 = 1; sp2 < nsplit; ++sp2) {
 #pragma unroll
-        for (int c = 0; c < NT; ++c)
-          if (c < mv) acc[c] = __fadd_rn(acc[c], __ldcg(p0 + ((size_t)sp2 * NT + c) * TC_BM + row));
+        for (int c = 0; c < NC; ++c)
+          if (cb + c < mv)
+            acc[c] = __fadd_rn(acc[c], __ldcg(p0 + ((size_t)sp2 * NT + cb + c) * TC_BM + row));
       }
       if (threadIdx.x == 0) a.tickets[tile] = 0;   // the next launch reuses it
     }
@@ -294,9 +301,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
       const uint32_t rbar = map_rank(&tail->red, 0);
       const uint32_t rbase = map_rank(red, 0);
 #pragma unroll
-      for (int c = 0; c < NT; ++c)
-        if (c < mv)
-          st_async_f32(rbase + (uint32_t)((((split - 1) * mv + c) * TC_BM + row) * 4), acc[c], rbar);
+      for (int c = 0; c < NC; ++c)
+        if (cb + c < mv)
+          st_async_f32(rbase + (uint32_t)((((split - 1) * mv + cb + c) * TC_BM + row) * 4), acc[c],
+                       rbar);
       return;
     }
     if (threadIdx.x == 0)
@@ -304,8 +312,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
     mbar_wait(&tail->red, 0);
     for (int sp2 = 1; sp2 < nsplit; ++sp2) {
 #pragma unroll
-      for (int c = 0; c < NT; ++c)
-        if (c < mv) acc[c] = __fadd_rn(acc[c], red[((sp2 - 1) * mv + c) * TC_BM + row]);
+      for (int c = 0; c < NC; ++c)
+        if (cb + c < mv) acc[c] = __fadd_rn(acc[c], red[((sp2 - 1) * mv + cb + c) * TC_BM + row]);
     }
   } else if (nsplit > 1) {
     // split-K merge through distributed shared memory: the nsplit CTAs of
@@ -314,7 +322,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
     // order straight from the peers' shared memory and runs the epilogue
     float* part = reinterpret_cast<float*>(smem);          // [NT][TC_BM]
 #pragma unroll
-    for (int c = 0; c < NT; ++c) part[c * TC_BM + row] = acc[c];
+    for (int c = 0; c < NC; ++c) part[(cb + c) * TC_BM + row] = acc[c];
     asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
                  "barrier.cluster.wait.acquire.aligned;" ::: "memory");
     uint32_t crank;
@@ -324,13 +332,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
       for (int sp2 = 1; sp2 < nsplit; ++sp2) {
         uint32_t ra;
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(sp2));
-        float v[NT];
+        float v[NC];
 #pragma unroll
-        for (int c = 0; c < NT; ++c)
+        for (int c = 0; c < NC; ++c)
           asm volatile("ld.shared::cluster.f32 %0, [%1];"
-                       : "=f"(v[c]) : "r"(ra + (uint32_t)((c * TC_BM + row) * 4)));
+                       : "=f"(v[c]) : "r"(ra + (uint32_t)(((cb + c) * TC_BM + row) * 4)));
 #pragma unroll
-        for (int c = 0; c < NT; ++c) acc[c] = __fadd_rn(acc[c], v[c]);
+        for (int c = 0; c < NC; ++c) acc[c] = __fadd_rn(acc[c], v[c]);
       }
     }
     // peers keep their shared memory alive until rank 0 has read it
@@ -357,12 +365,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
       inv = powf(a.rope_theta, -2.0f * (float)j / (float)hd);
     }
 #pragma unroll
-    for (int c = 0; c < NT; ++c) {
+    for (int c = 0; c < NC; ++c) {
+      const int cc = cb + c;
       float y = acc[c];
-      if (NORM) y = __fmul_rn(y, c < mv ? tail->inv_rms[c] : 0.f);
+      if (NORM) y = __fmul_rn(y, cc < mv ? tail->inv_rms[cc] : 0.f);
       const float partner = __shfl_xor_sync(0xffffffffu, y, 1);
-      if (c >= mv) continue;
-      const int t = a.tok0 + c;
+      if (cc >= mv) continue;
+      const int t = a.tok0 + cc;
       float o = y;
       if (sec < 2) {
         float sn, cs;
@@ -380,24 +389,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
   } else if (EPI == SP_EPI_SWIGLU) {
     const bool odd = (R & 1) != 0;
 #pragma unroll
-    for (int c = 0; c < NT; ++c) {
+    for (int c = 0; c < NC; ++c) {
+      const int cc = cb + c;
       float y = acc[c];
-      if (NORM) y = __fmul_rn(y, c < mv ? tail->inv_rms[c] : 0.f);
+      if (NORM) y = __fmul_rn(y, cc < mv ? tail->inv_rms[cc] : 0.f);
       const float up = __shfl_xor_sync(0xffffffffu, y, 1);
-      if (c >= mv || odd) continue;
-      const int t = a.tok0 + c;
+      if (cc >= mv || odd) continue;
+      const int t = a.tok0 + cc;
       reinterpret_cast<__nv_bfloat16*>(a.out)[(size_t)t * a.ldo + (R >> 1)] =
           __float2bfloat16_rn(__fmul_rn(silu(y), up));
     }
   } else if (EPI == SP_EPI_RESID) {
     float* x = reinterpret_cast<float*>(a.out);
     const float g = gnext;
-    float sq[NT];
+    float sq[NC];
 #pragma unroll
-    for (int c = 0; c < NT; ++c) {
+    for (int c = 0; c < NC; ++c) {
       sq[c] = 0.f;
-      if (c < mv) {
-        const int t = a.tok0 + c;
+      if (cb + c < mv) {
+        const int t = a.tok0 + cb + c;
         float* xp = x + (size_t)t * a.ldo + R;
         const float nv = __fadd_rn(XEARLY ? xold[XEARLY ? c : 0] : *xp, acc[c]);
         *xp = nv;
@@ -410,9 +420,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
     }
     // per-token sum of squares of this tile's 128 rows (fixed order)
 #pragma unroll
-    for (int c = 0; c < NT; ++c) {
+    for (int c = 0; c < NC; ++c) {
       const float s = warp_sum(sq[c]);
-      if (lane == 0) tail->ssw[warp][c] = s;
+      if (lane == 0) tail->ssw[q4][cb + c] = s;
     }
     __syncthreads();
     if (threadIdx.x < mv) {
@@ -428,17 +438,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
     // does not depend on scheduling or on how many tokens share the launch)
     float* tv = reinterpret_cast<float*>(smem);           // [NT][128]; stages are idle
 #pragma unroll
-    for (int c = 0; c < NT; ++c) {
-      if (c >= mv) break;
+    for (int c = 0; c < NC; ++c) {
+      const int cc = cb + c;
+      if (cc >= mv) break;
       float y = acc[c];
-      if (NORM) y = __fmul_rn(y, tail->inv_rms[c]);
-      tv[c * TC_BM + row] = y;
-      if (a.out) reinterpret_cast<float*>(a.out)[(size_t)(a.tok0 + c) * a.ldo + R] = y;
+      if (NORM) y = __fmul_rn(y, tail->inv_rms[cc]);
+      tv[cc * TC_BM + row] = y;
+      if (a.out) reinterpret_cast<float*>(a.out)[(size_t)(a.tok0 + cc) * a.ldo + R] = y;
     }
     __syncthreads();
     const int ntiles = gridDim.x;
     LmPartial* part = reinterpret_cast<LmPartial*>(a.lm_part);
-    for (int c = warp; c < mv; c += TC_THREADS / 32) {
+    for (int c = warp; c < mv; c += tc_threads(NT) / 32) {
       float v[4];
       TcTop2 t{-INFINITY, 0x7fffffff, -INFINITY, 0x7fffffff};
       float mx = -INFINITY;
@@ -464,7 +475,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
     __syncthreads();
     if (!tail->last) return;
     __threadfence();
-    for (int c = warp; c < mv; c += TC_THREADS / 32) {   // one warp per token
+    for (int c = warp; c < mv; c += tc_threads(NT) / 32) {   // one warp per token
       const LmPartial* P = part + (size_t)(a.tok0 + c) * ntiles;
       TcTop2 t{-INFINITY, 0x7fffffff, -INFINITY, 0x7fffffff};
       float mx = -INFINITY;
@@ -513,10 +524,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs a, const in
     }
   } else {  // SP_EPI_STORE
 #pragma unroll
-    for (int c = 0; c < mv; ++c) {
+    for (int c = 0; c < NC; ++c) {
+      const int cc = cb + c;
+      if (cc >= mv) break;
       float y = acc[c];
-      if (NORM) y = __fmul_rn(y, tail->inv_rms[c]);
-      reinterpret_cast<float*>(a.out)[(size_t)(a.tok0 + c) * a.ldo + R] = y;
+      if (NORM) y = __fmul_rn(y, tail->inv_rms[cc]);
+      reinterpret_cast<float*>(a.out)[(size_t)(a.tok0 + cc) * a.ldo + R] = y;
     }
   }
 }
@@ -588,7 +601,7 @@ static cudaError_t launch_nt(const CUtensorMap& x, const TcArgs& a, int ksplit,
   dim3 grid(a.n_rows / TC_BM, ksplit);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(tc_threads(NT));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
