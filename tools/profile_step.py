@@ -14,11 +14,12 @@ from paper_2407_11798_b200.engine import Engine, ExperimentConfig
 ap = argparse.ArgumentParser()
 ap.add_argument("--gen-len", type=int, default=16)
 ap.add_argument("--mode", default="async-speculative")
+ap.add_argument("--depth", type=int, default=3, help="speculation depth (bench N=1 default 3)")
 a = ap.parse_args()
 cfg = ExperimentConfig(mode="async-speculative", nodes=2, target_shape=B.TARGET,
                        draft_shape=B.DRAFT, draft_backend="synthetic", alpha=B.ALPHA,
                        prompt_len=B.PROMPT_LEN, gen_len=a.gen_len, max_context=B.MAX_CTX,
-                       target_seed=1, draft_seed=2)
+                       target_seed=1, draft_seed=2, microbatch=a.depth, tree_cap=a.depth)
 eng = Engine(cfg)
 for _ in range(2):
     eng.run(prompt_seed=1234, mode=a.mode)
