@@ -298,6 +298,11 @@ __global__ void __launch_bounds__(AT_THREADS) attn_tc_kernel(const AttnArgs a) {
                            ? (int)a.toks[ref].seq_mask : 0;
   const int nch = (ref_len + AT_C - 1) / AT_C;
   const int wz = blockIdx.y * NW + warp, W = gridDim.y * NW;   // this warp's chunks: wz + i*W
+  // row blocks (grid z, prefill-sized runs): this CTA's 16-row tiles
+  // [tb0, tb1); every (row, chunk) is still computed exactly once
+  const int ntiles = (nrows + 15) / 16;
+  const int tpb = (ntiles + gridDim.z - 1) / gridDim.z;
+  const int tb0 = blockIdx.z * tpb, tb1 = min(ntiles, tb0 + tpb);
   if ((int)blockIdx.y * NW >= nch) return;                      // no chunk for this CTA
   const int32_t* pref = a.vis + (size_t)ref * a.ld_vis;
   const int fresh0 = a.fresh_row0_dev ? *a.fresh_row0_dev : a.fresh_row0;
@@ -334,16 +339,18 @@ __global__ void __launch_bounds__(AT_THREADS) attn_tc_kernel(const AttnArgs a) {
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     return;
   }
-  if (blockIdx.y == 0 && tid == 0 && nch > a.nsplit) set_error(a.err, SP_DEV_PLAN_OVERFLOW);
+  if (blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && nch > a.nsplit)
+    set_error(a.err, SP_DEV_PLAN_OVERFLOW);
 
   for (int c = wz; c < nch; c += W) {
     issue(pref, ref_len, c, (c == wz && pre) ? 2 : 0);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
-    for (int t0 = 0; t0 < nrows; t0 += 16)
+    for (int t0 = tb0 * 16; t0 < tb1 * 16; t0 += 16)
       at_tile<HD>(a, kb, vb, c, t0, nrows, G, kh, 0, ref_mask, pref);
     // queries with a chunk of their own (tree siblings): one gather each
     for (int j = 0; j < a.n; ++j) {
+      if ((j * G) / 16 < tb0 || (j * G) / 16 >= tb1) continue;   // another row block's query
       const int gj = at_group(a, j, c, ref_mask, pref);
       if (gj != 1 + j) continue;
       __syncwarp();
@@ -492,7 +499,13 @@ static cudaError_t launch_tc_hd(const AttnArgs& a, cudaStream_t st) {
   const int per_sm = HD == 64 ? 3 : 1;
   const int chunks4 = (a.nsplit + 1) / 2 / (AT_THREADS / 32) + 1;   // (nsplit counts 32-entry splits)
   const int z = max(1, min(chunks4, (per_sm * 148 + a.KH - 1) / a.KH));
-  cudaError_t e = launch_pdl(attn_tc_kernel<HD>, dim3(a.KH, z), dim3(AT_THREADS), smem, st, a);
+  // many rows (prefill): their 16-row tiles spread over up to 8 row blocks
+  // (a warp otherwise walks every tile of its chunk in sequence); the
+  // in-kernel merge of <= 32 rows keeps one block
+  const int nrows = a.n * (a.H / a.KH);
+  static const int rb_max = getenv("SP_ATT_TC_RB") ? max(1, atoi(getenv("SP_ATT_TC_RB"))) : 8;
+  const int rb = nrows > AT_MERGE_ROWS ? max(1, min(rb_max, (nrows + 15) / 16)) : 1;
+  cudaError_t e = launch_pdl(attn_tc_kernel<HD>, dim3(a.KH, z, rb), dim3(AT_THREADS), smem, st, a);
   if (e != cudaSuccess || a.n * (a.H / a.KH) <= AT_MERGE_ROWS) return e;
   const size_t msmem = sizeof(float) * (size_t)a.nsplit;
   static size_t mconf = 0;

@@ -40,7 +40,7 @@ def plans_for(kind, ctx, n, gen):
 CASES = []
 for (H, KH, HD) in ((32, 32, 128), (16, 4, 64)):
     for kind in ("chain", "tree", "subset"):
-        for n in (1, 2, 5, 9, 16):
+        for n in (1, 2, 5, 9, 16, 40):   # (40: the tensor-core kernel)
             for ctx in (3, 31, 32, 33, 100, 384, 1000):
                 if kind != "chain" and n == 1:
                     continue

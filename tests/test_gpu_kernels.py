@@ -240,10 +240,12 @@ def test_tc_gemm_tile_size_invariance(env, shape):
 
 
 def test_attention_grid_and_merge_path_bitwise(tmp_path):
-    """The decode attention's bits do not depend on its grid or merge path
+    """The attention's bits do not depend on its grid or merge path
     (attention.cu attn_kernel): one split per CTA equals CTAs looping over
     several splits, and merging the split partials from shared memory
-    equals merging them from L2 -- on chains, tree siblings and arbitrary
+    equals merging them from L2; the tensor-core kernel (40-query runs,
+    attention_tc.cu) gives the same bits with its row tiles on one CTA or
+    spread over row blocks -- on chains, tree siblings and arbitrary
     per-query plans, head dims 64 / 128, GQA; every output is also checked
     against fp32 (model.py:394-415)."""
     import os
@@ -252,7 +254,8 @@ def test_attention_grid_and_merge_path_bitwise(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
     for name, extra in (("base", {}), ("loops", {"SP_ATT_CTAS_PER_SM": "1"}),
-                        ("l2merge", {"SP_ATT_MERGE_SMEM_KB": "0"})):
+                        ("l2merge", {"SP_ATT_MERGE_SMEM_KB": "0"}),
+                        ("tc_one_block", {"SP_ATT_TC_RB": "1"})):
         path = str(tmp_path / f"{name}.npz")
         env = dict(os.environ, **extra)
         r = subprocess.run([sys.executable, os.path.join(root, "tests", "attn_variant_main.py"),
@@ -260,6 +263,6 @@ def test_attention_grid_and_merge_path_bitwise(tmp_path):
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
         outs[name] = np.load(path)
     base = outs["base"]
-    for name in ("loops", "l2merge"):
+    for name in ("loops", "l2merge", "tc_one_block"):
         for key in base.files:
             assert np.array_equal(base[key], outs[name][key]), (name, key)
