@@ -339,3 +339,30 @@ def test_tree_speculation_matches_serial(world, mode, nodes):
             assert not head.allocator.live()          # every partition released
     if mode == "sync-speculative":
         assert per_run[2] > per_run[1]
+
+
+def test_common_prefix_matches_elementwise_scan():
+    """Head._common_prefix (slice compares) == the element-wise scan it
+    replaced, for lists and tuples, equal / prefix / diverging contexts."""
+    import random
+    from paper_2407_11798_b200.engine import Head
+
+    def scan(a, b):
+        n = 0
+        for x, y in zip(a, b):
+            if x != y:
+                break
+            n += 1
+        return n
+
+    rng = random.Random(7)
+    for _ in range(3000):
+        la, lb = rng.randint(0, 700), rng.randint(0, 700)
+        base = [rng.randint(0, 5) for _ in range(max(la, lb))]
+        a, b = base[:la], list(base[:lb])
+        if b and rng.random() < 0.6:
+            i = rng.randrange(len(b))
+            b[i] += 1
+        if rng.random() < 0.2:
+            b = tuple(b)
+        assert Head._common_prefix(a, b) == scan(a, b)
