@@ -1002,7 +1002,12 @@ class Head:
         fold = (alpha >= 0.5 and cheap) or alpha >= 0.75
         self.fold_frontier = fold
         if self.cfg.max_inflight is None:
-            self.max_inflight = self._fold_cap if fold else 0
+            # while chains break often, one run per stage plus one queued at
+            # the first (7B N=4, depth 2, alpha 0.66: cap 3 651 -> 4 685
+            # tok/s, 2 612, 6 634); long chains keep one per stage (alpha
+            # 0.9: 1472 at 3 vs 1438 at 4)
+            cap = self._fold_cap + (1 if alpha < 0.75 else 0)
+            self.max_inflight = cap if fold else 0
 
     def _frontier_carried(self) -> bool:
         pos = len(self.accepted) - 1
